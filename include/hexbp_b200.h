@@ -1,0 +1,142 @@
+/* include/hexbp_b200.h -- C ABI of the B200-native hexbp hot path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in the signatures;
+ * streams are passed as `void*` holding a cudaStream_t, NULL = legacy
+ * default stream). Every entry point names the reference interface it
+ * replaces (paths under /root/reference/proj/include/hexbp/).
+ *
+ * Status codes map to the reference's exception types:
+ *   HEXBP_OK                0
+ *   HEXBP_INVALID_ARGUMENT  1  std::invalid_argument   (e.g. operator.hpp:268)
+ *   HEXBP_DIVERGENCE        2  hexbp::divergence_error (solver.hpp:17-20,114,129-130,136)
+ *   HEXBP_CUDA_ERROR        3  std::runtime_error
+ *   HEXBP_OUT_OF_MEMORY     4  std::bad_alloc
+ *   HEXBP_DEGENERATE        5  hexbp::degenerate_element_error (geometry.hpp:19-32,129)
+ *   HEXBP_LOGIC             6  std::logic_error        (operator.hpp:258,284)
+ * A human-readable message for the last failure on the calling thread is
+ * returned by hexbp_last_error().
+ */
+#ifndef HEXBP_B200_H
+#define HEXBP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HEXBP_OK = 0,
+  HEXBP_INVALID_ARGUMENT = 1,
+  HEXBP_DIVERGENCE = 2,
+  HEXBP_CUDA_ERROR = 3,
+  HEXBP_OUT_OF_MEMORY = 4,
+  HEXBP_DEGENERATE = 5,
+  HEXBP_LOGIC = 6
+};
+
+typedef struct hexbp_setup_s* hexbp_setup_t;         /* device OperatorSetup (operator.hpp:60-68) */
+typedef struct hexbp_workspace_s* hexbp_workspace_t; /* device Workspace (operator.hpp:148-211)   */
+
+typedef struct {
+  int bp;            /* 1, 3 or 5 (BPKind, operator.hpp:29) */
+  int p, q;          /* degree, quadrature points per axis (operator.hpp:55) */
+  int dims[3];       /* local element counts */
+  int gdims[3];      /* global element counts (== dims unless a slab) */
+  int z0;            /* first global element layer of this slab */
+  int components;    /* 1 (BP1 wdetJ) or 6 (BP3/BP5 G) (geometry.hpp:41-57) */
+  int64_t l_size;    /* OperatorSetup::l_size (operator.hpp:66) */
+  int64_t elements;  /* OperatorSetup::num_elements (operator.hpp:67) */
+  int64_t factor_bytes;
+} hexbp_setup_info;
+
+typedef struct {
+  int iterations;            /* CGReport::iterations       (solver.hpp:76-82) */
+  int converged;             /* CGReport::converged        */
+  double final_rel_residual; /* CGReport::final_rel_residual */
+  double r0_norm;            /* residual_history[0]        */
+  double seconds;            /* CGReport::seconds (host wall clock of the call) */
+} hexbp_cg_report;
+
+const char* hexbp_last_error(void);
+int hexbp_device_count(void);
+
+/* Replaces make_setup(kind, mesh) for the reference's structured box mesh
+ * (operator.hpp:70-77, mesh.hpp:86-123, geometry.hpp:78-193): the mesh
+ * coordinates, Jacobians and geometric factors are generated ON THE DEVICE
+ * with the reference's operation order. extent = NULL means {1,1,1}. */
+int hexbp_setup_create_box(int bp, int p, const int dims[3], const double extent[3], double amplitude,
+                           int device, hexbp_setup_t* out);
+
+/* Slab of the same global box (z element layers [z0, z1)) for the multi-GPU
+ * partition; its node planes are [z0*p, z1*p] of the global grid. */
+int hexbp_setup_create_box_slab(int bp, int p, const int gdims[3], int z0, int z1, const double extent[3],
+                                double amplitude, int device, hexbp_setup_t* out);
+
+/* Replaces an existing host OperatorSetup: uploads the reference's own
+ * tables -- B, D (q x (p+1) row-major, basis.hpp:21-22) and the factors in
+ * the reference AoS layout data[(e*q^3+qp)*comp + c] (geometry.hpp:48-56) --
+ * and re-lays them out for the device kernel. */
+int hexbp_setup_create(int bp, int p, int q, const int dims[3], const double* B, const double* D,
+                       const double* factors_aos, int device, hexbp_setup_t* out);
+
+void hexbp_setup_destroy(hexbp_setup_t s);
+int hexbp_setup_get_info(hexbp_setup_t s, hexbp_setup_info* out);
+/* B, D as used by the kernels (q x (p+1) row-major). */
+int hexbp_setup_basis(hexbp_setup_t s, double* B, double* D);
+/* Factors downloaded back into the reference AoS layout (validation). */
+int hexbp_setup_factors(hexbp_setup_t s, double* factors_aos);
+
+/* Replaces OperatorHandle::make_workspace (operator.hpp:262): ticket/progress
+ * flags, per-column partial sums, CG vectors and scalars. All device memory
+ * is allocated here; apply and cg never allocate. */
+int hexbp_workspace_create(hexbp_setup_t s, hexbp_workspace_t* out);
+void hexbp_workspace_destroy(hexbp_workspace_t ws);
+
+/* Replaces OperatorHandle::apply(u, w, ws) (operator.hpp:265-279) and, with
+ * constrained = 1, ConstrainedOperator::apply (solver.hpp:60-65). Device
+ * pointers of l_size doubles, asynchronous on `stream`. u and w must not
+ * alias. */
+int hexbp_apply(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, double* w_dev, int constrained,
+                void* stream);
+
+/* Same, with HOST buffers of n doubles; synchronous (drop-in for the
+ * reference's std::span / std::vector signature). */
+int hexbp_apply_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* u, double* w, int64_t n, int constrained);
+
+/* Replaces cg(apply, b, x, rel_tol, max_iter) (solver.hpp:91-153) for a device
+ * operator: the whole recurrence runs on the device (fused AXPY + fixed-order
+ * reductions, p.Ap fused into the operator kernel). b_dev, x_dev: l_size
+ * doubles on the device; x_dev holds x0 on entry. `history` (host, may be
+ * NULL) receives residual_history (iterations+1 entries, capacity
+ * max_iter+1). Synchronous. */
+int hexbp_cg(hexbp_setup_t s, hexbp_workspace_t ws, const double* b_dev, double* x_dev, double rel_tol, int max_iter,
+             int constrained, hexbp_cg_report* report, double* history, void* stream);
+
+/* Same with HOST b and x (x0 in, solution out). */
+int hexbp_cg_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* b, double* x, int64_t n, double rel_tol,
+                  int max_iter, int constrained, hexbp_cg_report* report, double* history);
+
+/* deterministic_dot (dense.hpp:74-81) on device vectors: fixed-order
+ * partition, bitwise reproducible run to run. Synchronous. */
+int hexbp_dot(hexbp_workspace_t ws, const double* a_dev, const double* b_dev, int64_t n, double* out, void* stream);
+
+/* OperatorHandle::count_flops (operator.hpp:283-294): per-element multiplies
+ * and adds executed by the device kernel (analytic trip counts). */
+int hexbp_count_flops(hexbp_setup_t s, uint64_t* mul, uint64_t* add);
+
+/* Seeded right-hand side of the reference benchmark (bench.hpp:234-243,
+ * seed mixing bench.hpp:193-204; BENCH_SEED default 20240101): entries
+ * [offset, offset+count) of the global L-vector of the (bp, p, dims) box,
+ * boundary dofs zeroed for BP3/BP5. Generated with the same std::mt19937_64 /
+ * uniform_real_distribution so the device solves the reference's system. */
+int hexbp_bench_rhs(int bp, int p, const int dims[3], uint64_t seed, int64_t offset, int64_t count, double* out);
+
+/* Kernel resource report: registers/thread, static+dynamic smem bytes,
+ * threads per CTA, resident CTAs per SM. */
+int hexbp_kernel_info(hexbp_setup_t s, int* regs, int* smem_bytes, int* threads, int* ctas_per_sm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXBP_B200_H */

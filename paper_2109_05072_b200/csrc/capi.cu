@@ -1,0 +1,499 @@
+// C ABI of the B200 hot path (include/hexbp_b200.h): setup / workspace
+// lifetime, operator apply, device-resident CG, deterministic dot.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+struct hexbp_setup_s {
+  hxb::Setup s;
+};
+struct hexbp_workspace_s {
+  hxb::Workspace w;
+};
+
+namespace hxb {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace hxb
+
+using namespace hxb;
+
+namespace {
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HEXBP_OK;
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  cudaGetLastError();  // clear sticky non-fatal errors
+  return e == cudaErrorMemoryAllocation ? HEXBP_OUT_OF_MEMORY : HEXBP_CUDA_ERROR;
+}
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_status(_e, #call); \
+  } while (0)
+
+int invalid(const std::string& m) {
+  set_error(m);
+  return HEXBP_INVALID_ARGUMENT;
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int kind_of(int bp) { return bp == 1 ? KIND_MASS : (bp == 3 ? KIND_DIFF : KIND_COLLOC); }
+
+int default_q(int bp, int p) { return bp == 5 ? p + 1 : p + 2; }  // operator.hpp:55
+
+int init_setup(Setup& s, int bp, int p, const int gdims[3], int z0, int z1, int device) {
+  if (!(bp == 1 || bp == 3 || bp == 5)) return invalid("setup: bp must be 1, 3 or 5");
+  if (p < 1 || p > kMaxP) return invalid("setup: degree must be in [1, 8] for the device kernels");
+  for (int d = 0; d < 3; ++d)
+    if (gdims[d] < 1) return invalid("build_box_mesh: element counts must be >= 1");
+  if (z0 < 0 || z1 <= z0 || z1 > gdims[2]) return invalid("setup: bad slab range");
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  if (ndev == 0) {
+    set_error("no CUDA device available: the hexbp-b200 operator has no CPU fallback");
+    return HEXBP_CUDA_ERROR;
+  }
+  if (device < 0 || device >= ndev) return invalid("setup: bad device ordinal");
+  s.bp = bp;
+  s.p = p;
+  s.q = default_q(bp, p);
+  s.kind = kind_of(bp);
+  s.comp = bp == 1 ? 1 : 6;
+  for (int d = 0; d < 3; ++d) s.gdims[d] = gdims[d];
+  s.dims[0] = gdims[0];
+  s.dims[1] = gdims[1];
+  s.dims[2] = z1 - z0;
+  s.z0 = z0;
+  s.bc_zlo = z0 == 0;
+  s.bc_zhi = z1 == gdims[2];
+  s.device = device;
+  s.nL = static_cast<int64_t>(s.dims[0] * p + 1) * (s.dims[1] * p + 1) * (s.dims[2] * p + 1);
+  s.E = static_cast<int64_t>(s.dims[0]) * s.dims[1] * s.dims[2];
+  const long long per = static_cast<long long>(s.comp) * s.q * s.q * s.q;
+  s.gstride = (per + 1) / 2 * 2;
+  std::vector<double> qp(s.q), npn(p + 1), nw(p + 1);
+  try {
+    build_basis(p, s.q, bp == 5, s.B, s.D, qp.data(), s.qw, npn.data(), nw.data());
+  } catch (const std::exception& e) {
+    return invalid(e.what());
+  }
+  return HEXBP_OK;
+}
+
+int create_box(int bp, int p, const int gdims[3], int z0, int z1, const double extent[3], double amplitude,
+               int device, hexbp_setup_t* out) {
+  if (!out) return invalid("setup: null output handle");
+  *out = nullptr;
+  const double ext[3] = {extent ? extent[0] : 1.0, extent ? extent[1] : 1.0, extent ? extent[2] : 1.0};
+  for (int d = 0; d < 3; ++d)
+    if (!(ext[d] > 0.0)) return invalid("build_box_mesh: extents must be positive");
+  if (!(amplitude >= 0.0 && amplitude <= 0.15))  // mesh.hpp:84,104-105
+    return invalid("build_box_mesh: deform amplitude outside [0, 0.15]");
+  auto* h = new (std::nothrow) hexbp_setup_s;
+  if (!h) return HEXBP_OUT_OF_MEMORY;
+  Setup& s = h->s;
+  int rc = init_setup(s, bp, p, gdims, z0, z1, device);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  DeviceGuard g(device);
+  // Global axis coordinates and the separable deformation factors, on the
+  // host with libm exactly as mesh.hpp:59-67,107-116 evaluates them.
+  constexpr double kPi = 3.141592653589793;
+  std::vector<double> axis[3], sn[3];
+  for (int d = 0; d < 3; ++d) {
+    axis[d] = axis_node_coords(gdims[d], p, ext[d]);
+    sn[d].resize(axis[d].size());
+    for (std::size_t i = 0; i < axis[d].size(); ++i) sn[d][i] = std::sin(2.0 * kPi * axis[d][i] / ext[d]);
+  }
+  double* dbuf = nullptr;
+  std::size_t tot = 0;
+  for (int d = 0; d < 3; ++d) tot += 2 * axis[d].size();
+  const std::size_t gbytes = sizeof(double) * static_cast<std::size_t>(s.gstride) * s.E;
+  cudaError_t e = cudaMalloc(&s.G, gbytes);
+  if (e) {
+    delete h;
+    return cuda_status(e, "cudaMalloc(factors)");
+  }
+  unsigned long long* bad = nullptr;
+  double* bad_det = nullptr;
+  e = cudaMalloc(&dbuf, sizeof(double) * tot + 16 + sizeof(double));
+  if (e) {
+    cudaFree(s.G);
+    delete h;
+    return cuda_status(e, "cudaMalloc(axis)");
+  }
+  std::vector<double> host(tot);
+  BoxGeometryArgs ga{};
+  std::size_t off = 0;
+  const double** ap[3] = {&ga.ax, &ga.ay, &ga.az};
+  const double** sp[3] = {&ga.sx, &ga.sy, &ga.sz};
+  for (int d = 0; d < 3; ++d) {
+    std::memcpy(host.data() + off, axis[d].data(), sizeof(double) * axis[d].size());
+    *ap[d] = dbuf + off;
+    off += axis[d].size();
+    std::memcpy(host.data() + off, sn[d].data(), sizeof(double) * sn[d].size());
+    *sp[d] = dbuf + off;
+    off += sn[d].size();
+  }
+  ga.amplitude = amplitude;
+  for (int d = 0; d < 3; ++d) ga.ext[d] = ext[d];
+  bad = reinterpret_cast<unsigned long long*>(dbuf + tot);
+  bad_det = dbuf + tot + 2;
+  cudaMemcpy(dbuf, host.data(), sizeof(double) * tot, cudaMemcpyHostToDevice);
+  cudaMemset(bad, 0xff, sizeof(unsigned long long));
+  e = launch_box_geometry(s, ga, bad, bad_det, nullptr);
+  if (!e) e = cudaDeviceSynchronize();
+  unsigned long long hbad = ~0ull;
+  double hdet = 0.0;
+  if (!e) {
+    cudaMemcpy(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&hdet, bad_det, sizeof hdet, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dbuf);
+  if (e) {
+    cudaFree(s.G);
+    delete h;
+    return cuda_status(e, "box geometry");
+  }
+  if (hbad != ~0ull) {
+    const long long elem = static_cast<long long>(hbad >> 20);
+    const int qpt = static_cast<int>(hbad & 0xfffff);
+    set_error("non-positive Jacobian determinant " + std::to_string(hdet) + " at element " + std::to_string(elem) +
+              ", quadrature point " + std::to_string(qpt));
+    cudaFree(s.G);
+    delete h;
+    return HEXBP_DEGENERATE;
+  }
+  *out = h;
+  return HEXBP_OK;
+}
+
+int ensure_host_staging(Workspace& w) {
+  if (w.tmp_u) return HEXBP_OK;
+  CK(cudaMalloc(&w.tmp_u, sizeof(double) * w.s->nL));
+  CK(cudaMalloc(&w.tmp_w, sizeof(double) * w.s->nL));
+  return HEXBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hexbp_last_error(void) { return g_last_error.c_str(); }
+
+int hexbp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int hexbp_setup_create_box(int bp, int p, const int dims[3], const double extent[3], double amplitude, int device,
+                           hexbp_setup_t* out) {
+  if (!dims) return invalid("setup: null dims");
+  return create_box(bp, p, dims, 0, dims[2], extent, amplitude, device, out);
+}
+
+int hexbp_setup_create_box_slab(int bp, int p, const int gdims[3], int z0, int z1, const double extent[3],
+                                double amplitude, int device, hexbp_setup_t* out) {
+  if (!gdims) return invalid("setup: null dims");
+  return create_box(bp, p, gdims, z0, z1, extent, amplitude, device, out);
+}
+
+int hexbp_setup_create(int bp, int p, int q, const int dims[3], const double* B, const double* D,
+                       const double* factors_aos, int device, hexbp_setup_t* out) {
+  if (!out || !dims || !B || !D || !factors_aos) return invalid("setup: null argument");
+  *out = nullptr;
+  auto* h = new (std::nothrow) hexbp_setup_s;
+  if (!h) return HEXBP_OUT_OF_MEMORY;
+  Setup& s = h->s;
+  int rc = init_setup(s, bp, p, dims, 0, dims[2], device);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  if (q != s.q) {
+    delete h;
+    return invalid("setup: the device kernels implement the reference quadrature convention q = p+2 (BP1/BP3), "
+                   "p+1 (BP5) (operator.hpp:55)");
+  }
+  const int n = p + 1;
+  std::memcpy(s.B, B, sizeof(double) * q * n);
+  std::memcpy(s.D, D, sizeof(double) * q * n);
+  DeviceGuard g(device);
+  const std::size_t aos_n = static_cast<std::size_t>(s.E) * q * q * q * s.comp;
+  double* tmp = nullptr;
+  cudaError_t e = cudaMalloc(&s.G, sizeof(double) * static_cast<std::size_t>(s.gstride) * s.E);
+  if (!e) e = cudaMalloc(&tmp, sizeof(double) * aos_n);
+  if (!e) e = cudaMemcpy(tmp, factors_aos, sizeof(double) * aos_n, cudaMemcpyHostToDevice);
+  if (!e) e = launch_factors_from_aos(s, tmp, nullptr);
+  if (!e) e = cudaDeviceSynchronize();
+  if (tmp) cudaFree(tmp);
+  if (e) {
+    if (s.G) cudaFree(s.G);
+    delete h;
+    return cuda_status(e, "setup upload");
+  }
+  *out = h;
+  return HEXBP_OK;
+}
+
+void hexbp_setup_destroy(hexbp_setup_t h) {
+  if (!h) return;
+  DeviceGuard g(h->s.device);
+  if (h->s.G) cudaFree(h->s.G);
+  delete h;
+}
+
+int hexbp_setup_get_info(hexbp_setup_t h, hexbp_setup_info* out) {
+  if (!h || !out) return invalid("null argument");
+  const Setup& s = h->s;
+  out->bp = s.bp;
+  out->p = s.p;
+  out->q = s.q;
+  for (int d = 0; d < 3; ++d) {
+    out->dims[d] = s.dims[d];
+    out->gdims[d] = s.gdims[d];
+  }
+  out->z0 = s.z0;
+  out->components = s.comp;
+  out->l_size = s.nL;
+  out->elements = s.E;
+  out->factor_bytes = static_cast<int64_t>(s.E) * s.q * s.q * s.q * s.comp * 8;
+  return HEXBP_OK;
+}
+
+int hexbp_setup_basis(hexbp_setup_t h, double* B, double* D) {
+  if (!h || !B || !D) return invalid("null argument");
+  const int nq = h->s.q * (h->s.p + 1);
+  std::memcpy(B, h->s.B, sizeof(double) * nq);
+  std::memcpy(D, h->s.D, sizeof(double) * nq);
+  return HEXBP_OK;
+}
+
+int hexbp_setup_factors(hexbp_setup_t h, double* aos) {
+  if (!h || !aos) return invalid("null argument");
+  const Setup& s = h->s;
+  DeviceGuard g(s.device);
+  const std::size_t n = static_cast<std::size_t>(s.E) * s.q * s.q * s.q * s.comp;
+  double* tmp = nullptr;
+  CK(cudaMalloc(&tmp, sizeof(double) * n));
+  cudaError_t e = launch_factors_to_aos(s, tmp, nullptr);
+  if (!e) e = cudaMemcpy(aos, tmp, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  return cuda_status(e, "factors download");
+}
+
+int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
+  if (!h || !out) return invalid("null argument");
+  *out = nullptr;
+  auto* wh = new (std::nothrow) hexbp_workspace_s;
+  if (!wh) return HEXBP_OUT_OF_MEMORY;
+  Workspace& w = wh->w;
+  const Setup& s = h->s;
+  w.s = &s;
+  w.device = s.device;
+  DeviceGuard g(s.device);
+  const int ncols = s.dims[0] * s.dims[1];
+  const std::size_t n = static_cast<std::size_t>(s.nL);
+  w.vec_blocks = vec_grid(s.nL);
+  w.history_cap = 4097;
+  cudaError_t e = cudaSuccess;
+  auto al = [&](void** p, std::size_t bytes) {
+    if (!e) e = cudaMalloc(p, bytes);
+    if (!e) e = cudaMemset(*p, 0, bytes);
+  };
+  al(reinterpret_cast<void**>(&w.sync), sizeof(ApplySync));
+  al(reinterpret_cast<void**>(&w.progress), sizeof(unsigned long long) * ncols);
+  al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * ncols);
+  al(reinterpret_cast<void**>(&w.sc), sizeof(DevScalars));
+  al(reinterpret_cast<void**>(&w.r), sizeof(double) * n);
+  al(reinterpret_cast<void**>(&w.p), sizeof(double) * n);
+  al(reinterpret_cast<void**>(&w.Ap), sizeof(double) * n);
+  al(reinterpret_cast<void**>(&w.vec_partials), sizeof(double) * (148 * 8 + 8));
+  al(reinterpret_cast<void**>(&w.vec_done), sizeof(unsigned int) * 4);
+  al(reinterpret_cast<void**>(&w.history), sizeof(double) * w.history_cap);
+  if (!e) e = cudaMallocHost(reinterpret_cast<void**>(&w.host_sc), sizeof(DevScalars));
+  if (e) {
+    hexbp_workspace_destroy(wh);
+    return cuda_status(e, "workspace allocation");
+  }
+  w.apply_grid = apply_occupancy_grid(s);
+  *out = wh;
+  return HEXBP_OK;
+}
+
+void hexbp_workspace_destroy(hexbp_workspace_t wh) {
+  if (!wh) return;
+  Workspace& w = wh->w;
+  DeviceGuard g(w.device);
+  void* bufs[] = {w.sync, w.progress, w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
+                  w.vec_done, w.history};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (w.host_sc) cudaFreeHost(w.host_sc);
+  delete wh;
+}
+
+int hexbp_apply(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* w, int constrained, void* stream) {
+  if (!h || !wh || !u || !w) return invalid("apply: null argument");
+  if (wh->w.s != &h->s) return invalid("apply: workspace belongs to another setup");
+  if (u == w) return invalid("apply: u and w must not alias");
+  DeviceGuard g(h->s.device);
+  CK(launch_apply(h->s, wh->w, u, w, constrained, nullptr, nullptr, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_apply_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* w, int64_t n, int constrained) {
+  if (!h || !wh || !u || !w) return invalid("apply: null argument");
+  if (n != h->s.nL) return invalid("apply: L-vector length mismatch");  // operator.hpp:268
+  DeviceGuard g(h->s.device);
+  Workspace& ws = wh->w;
+  int rc = ensure_host_staging(ws);
+  if (rc) return rc;
+  CK(cudaMemcpy(ws.tmp_u, u, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(launch_apply(h->s, ws, ws.tmp_u, ws.tmp_w, constrained, nullptr, nullptr, nullptr));
+  CK(cudaMemcpy(w, ws.tmp_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return HEXBP_OK;
+}
+
+int hexbp_cg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, double rel_tol, int max_iter,
+             int constrained, hexbp_cg_report* report, double* history, void* stream) {
+  if (!h || !wh || !b || !x) return invalid("cg: null argument");
+  if (max_iter < 0) return invalid("cg: max_iter must be >= 0");
+  const auto t0 = std::chrono::steady_clock::now();
+  const Setup& s = h->s;
+  Workspace& w = wh->w;
+  DeviceGuard g(s.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (max_iter + 1 > w.history_cap) {
+    CK(cudaFree(w.history));
+    w.history = nullptr;
+    w.history_cap = max_iter + 1;
+    CK(cudaMalloc(&w.history, sizeof(double) * w.history_cap));
+  }
+  const int64_t n = s.nL;
+  // r0 = b - A x0 (solver.hpp:102-103)
+  CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
+  CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
+  const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
+  for (int k = 1; k <= max_iter; ++k) {
+    CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st));
+    CK(launch_cg_update_r(w, n, st));
+    CK(launch_cg_update_xp(w, x, n, st));
+    if (k % check_every == 0 && k < max_iter) {
+      CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (w.host_sc->status != ST_RUNNING) break;
+    }
+  }
+  CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const DevScalars hs = *w.host_sc;
+  if (history) CK(cudaMemcpy(history, w.history, sizeof(double) * (hs.iterations + 1), cudaMemcpyDeviceToHost));
+  if (report) {
+    double last = hs.r0;
+    if (hs.iterations > 0) CK(cudaMemcpy(&last, w.history + hs.iterations, sizeof(double), cudaMemcpyDeviceToHost));
+    report->iterations = hs.iterations;
+    report->converged = hs.status == ST_CONVERGED;
+    report->r0_norm = hs.r0;
+    report->final_rel_residual = hs.r0 == 0.0 ? 0.0 : last / hs.r0;
+    report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  if (hs.status == ST_DIVERGED) {
+    set_error(hs.iterations == 0 && !std::isfinite(hs.r0) ? "cg: non-finite initial residual"
+                                                          : "cg: operator not positive definite on the search space "
+                                                            "or non-finite residual");
+    return HEXBP_DIVERGENCE;
+  }
+  return HEXBP_OK;
+}
+
+int hexbp_cg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, int64_t n, double rel_tol,
+                  int max_iter, int constrained, hexbp_cg_report* report, double* history) {
+  if (!h || !wh || !b || !x) return invalid("cg: null argument");
+  if (n != h->s.nL) return invalid("cg: x0 length mismatch");  // solver.hpp:96
+  DeviceGuard g(h->s.device);
+  Workspace& w = wh->w;
+  int rc = ensure_host_staging(w);
+  if (rc) return rc;
+  CK(cudaMemcpy(w.tmp_u, b, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(w.tmp_w, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  rc = hexbp_cg(h, wh, w.tmp_u, w.tmp_w, rel_tol, max_iter, constrained, report, history, nullptr);
+  if (rc == HEXBP_OK || rc == HEXBP_DIVERGENCE) CK(cudaMemcpy(x, w.tmp_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return rc;
+}
+
+int hexbp_dot(hexbp_workspace_t wh, const double* a, const double* b, int64_t n, double* out, void* stream) {
+  if (!wh || !a || !b || !out) return invalid("dot: null argument");
+  Workspace& w = wh->w;
+  DeviceGuard g(w.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* dres = w.vec_partials + 148 * 8;
+  CK(launch_dot(w, a, b, n, dres, st));
+  CK(cudaMemcpyAsync(out, dres, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return HEXBP_OK;
+}
+
+int hexbp_count_flops(hexbp_setup_t h, uint64_t* mul, uint64_t* add) {
+  if (!h || !mul || !add) return invalid("null argument");
+  const uint64_t N = h->s.p + 1, Q = h->s.q;
+  uint64_t fma = 0, m = 0, a = 0;
+  switch (h->s.kind) {
+    case KIND_DIFF:
+      fma = 4 * N * N * N * Q + 6 * N * N * Q * Q + 6 * N * Q * Q * Q;
+      m = 9 * Q * Q * Q;
+      a = 6 * Q * Q * Q;
+      break;
+    case KIND_COLLOC:
+      fma = 6 * N * N * N * N;
+      m = 9 * N * N * N;
+      a = 6 * N * N * N + 2 * N * N * N;  // + the identity-branch adds of Y'/Z'
+      break;
+    default:
+      fma = 2 * (N * N * N * Q + N * N * Q * Q + N * Q * Q * Q);
+      m = Q * Q * Q;
+      break;
+  }
+  *mul = fma + m;
+  *add = fma + a;
+  return HEXBP_OK;
+}
+
+int hexbp_kernel_info(hexbp_setup_t h, int* regs, int* smem, int* threads, int* ctas) {
+  if (!h || !regs || !smem || !threads || !ctas) return invalid("null argument");
+  DeviceGuard g(h->s.device);
+  apply_kernel_info(h->s, regs, smem, threads, ctas);
+  return HEXBP_OK;
+}
+
+}  // extern "C"

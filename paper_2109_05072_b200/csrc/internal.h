@@ -1,0 +1,131 @@
+// Internal declarations shared by the hexbp-b200 translation units.
+// Public C ABI: include/hexbp_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hexbp_b200.h"
+
+namespace hxb {
+
+// Element kernel families (operator.hpp:29,51,55-56):
+//   MASS   = BP1, q = p+2 Gauss, one factor per point (wdetJ)
+//   DIFF   = BP3, q = p+2 Gauss, six factors per point (G)
+//   COLLOC = BP5, q = p+1 GLL (B = I exactly, basis.hpp:55-66), six factors
+enum Kind : int { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
+
+constexpr int kMaxP = 8;
+constexpr int kMaxQ = kMaxP + 2;
+
+// Device-resident CG state (solver.hpp:91-153); read/written only by kernels.
+struct DevScalars {
+  double rz, pAp, alpha, beta, r0, rnorm, rel_tol, pad0;
+  int status, iterations, x_pending, max_iter;
+};
+enum : int { ST_RUNNING = 0, ST_CONVERGED = 1, ST_DIVERGED = 2, ST_MAXITER = 3 };
+
+// Column-ticket bookkeeping of the fused apply kernel (see apply.cu).
+struct ApplySync {
+  unsigned int ticket, done, epoch, pad;
+};
+
+// Arguments of the fused operator kernel (passed by value, __grid_constant__).
+struct ApplyArgs {
+  const double* u;
+  double* w;
+  const double* G;          // factors, device layout (setup.cu)
+  long long gstride;        // doubles per element block of G
+  int nx, ny, nz;           // elements of this (slab) mesh
+  int Nx, Ny, Nz;           // local node grid
+  int ncols;                // nx * ny
+  int constrained;          // ConstrainedOperator semantics (solver.hpp:60-65)
+  int bc_zlo, bc_zhi;       // z-faces that are essential (slab partitions)
+  ApplySync* sync;
+  unsigned long long* progress;  // per column
+  double* col_dot;          // per-column partial p.Ap (nullptr: no dot)
+  DevScalars* sc;           // CG scalars (nullptr: plain apply)
+  double* dot_out;          // where the final dot lands (nullptr: CG alpha logic only)
+};
+
+struct Setup {
+  int bp = 3, p = 1, q = 3, kind = KIND_DIFF, comp = 6;
+  int dims[3] = {1, 1, 1};   // local element counts
+  int gdims[3] = {1, 1, 1};  // global element counts
+  int z0 = 0;                // first global element layer of this slab
+  int bc_zlo = 1, bc_zhi = 1;
+  int64_t nL = 0;
+  int64_t E = 0;
+  int device = 0;
+  long long gstride = 0;
+  double B[kMaxQ * (kMaxP + 1)] = {};
+  double D[kMaxQ * (kMaxP + 1)] = {};
+  double qw[kMaxQ] = {};
+  double* G = nullptr;  // device
+};
+
+struct Workspace {
+  const Setup* s = nullptr;
+  int device = 0;
+  ApplySync* sync = nullptr;
+  unsigned long long* progress = nullptr;
+  double* col_dot = nullptr;
+  DevScalars* sc = nullptr;
+  double* r = nullptr;
+  double* p = nullptr;
+  double* Ap = nullptr;
+  double* tmp_u = nullptr;  // host-API staging
+  double* tmp_w = nullptr;
+  double* vec_partials = nullptr;
+  unsigned int* vec_done = nullptr;
+  double* history = nullptr;
+  int history_cap = 0;
+  int vec_blocks = 0;
+  int apply_grid = 0;
+  DevScalars* host_sc = nullptr;  // pinned mirror
+};
+
+// ---- apply.cu
+cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                         double* dot_out, DevScalars* sc, cudaStream_t st);
+int apply_occupancy_grid(const Setup& s);
+void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm);
+
+// ---- cg.cu
+cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
+                           cudaStream_t st);
+cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st);
+cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st);
+cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
+                       cudaStream_t st);
+int vec_grid(int64_t n);
+
+// ---- setup.cu
+struct BoxGeometryArgs {
+  const double* ax;  // axis node coordinates (global index)
+  const double* ay;
+  const double* az;
+  const double* sx;  // sin(2 pi x / Lx) per axis node, host libm (mesh.hpp:107-116)
+  const double* sy;
+  const double* sz;
+  double amplitude;
+  double ext[3];
+};
+cudaError_t launch_box_geometry(const Setup& s, const BoxGeometryArgs& g, unsigned long long* bad_key,
+                                double* bad_det, cudaStream_t st);
+cudaError_t launch_factors_from_aos(const Setup& s, const double* aos, cudaStream_t st);
+cudaError_t launch_factors_to_aos(const Setup& s, double* aos, cudaStream_t st);
+
+// ---- basis.cpp (host)
+void gl_rule(int n, double* pts, double* wts);
+void gll_rule(int n, double* pts, double* wts);
+void build_basis(int p, int q, bool gll, double* B, double* D, double* qpts, double* qwts, double* npts,
+                 double* nwts);
+std::vector<double> axis_node_coords(int elems, int p, double length);
+
+void set_error(const std::string& msg);
+
+}  // namespace hxb

@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark: BP3 GDOF/s (DOFs x CG iterations / s) of the device-resident CG
+on the reference's bench problem, plus the HBM-roofline fraction of the fused
+operator kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--bp 3] [--p 7] [--dims 66,66,66]
+
+A "step" is one CG iteration (operator apply + fused vector updates) over the
+whole mesh; the timed region is one fixed-iteration solve of K iterations
+(rel_tol = 0, exactly the reference's run_bench protocol, bench.hpp:251-267,
+including the initial residual), inputs already resident in HBM. Default
+workload = BASELINE config 3: BP3, Q_7, 66^3 elements, 99,252,847 DOFs, fp64.
+The geometric factors (10 GB) exceed L2 (126 MB), so every timed iteration
+streams from HBM (no L2 flush needed).
+
+N > 1 (torchrun, one rank per GPU): weak scaling; rank r owns the z-slab
+[r*ez, (r+1)*ez) of a (ex, ey, N*ez) box; the interface-plane halo sum and the
+CG dot products go over NCCL (paper_2109_05072_b200/parallel.py).
+
+--impl reference times the reference's own CPU implementation (the
+unmodified headers compiled in place, oracle/_ref) on this host's cores with
+all threads, on a bounded sample of the same workload (same bp/p, smaller mesh).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BP3 GDOF/s (DOFs x CG iters/sec), fp64, % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bp", type=int, default=3)
+    ap.add_argument("--p", type=int, default=7)
+    ap.add_argument("--dims", default=None, help="ex,ey,ez per GPU (default 66,66,66 for p=7)")
+    ap.add_argument("--amplitude", type=float, default=0.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    return ap.parse_args()
+
+
+def default_dims(p: int):
+    # ~100M DOFs per GPU: (e*p+1)^3 <= 1e8 (auto_size_dims, bench.hpp:179-187)
+    e = 1
+    while ((e + 1) * p + 1) ** 3 <= 100_000_000:
+        e += 1
+    return (e, e, e)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(bp: int, p: int, dims):
+    """per apply 8(c E q^3 + 2 n_L); per CG iteration 8(c E q^3 + 10 n_L)."""
+    q = p + 1 if bp == 5 else p + 2
+    c = 1 if bp == 1 else 6
+    E = dims[0] * dims[1] * dims[2]
+    nL = (dims[0] * p + 1) * (dims[1] * p + 1) * (dims[2] * p + 1)
+    return 8 * (c * E * q**3 + 2 * nL), 8 * (c * E * q**3 + 10 * nL), nL, E
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(bp: int, p: int, steps: int = 3):
+    """The reference's own run_bench (oracle/_ref) on this host, all cores,
+    bounded sample: same bp/p on ~2M DOFs, fixed CG iterations."""
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    e = 1
+    while ((e + 1) * p + 1) ** 3 <= 2_000_000:
+        e += 1
+    cfg = {"bp": f"bp{bp}", "degrees": [p], "dims": [e, e, e], "backends": ["fused"], "fixed_cg_iters": steps,
+           "warmup_repeats": 1, "timed_repeats": 2, "threads": cores}
+    kind = "reference"
+    try:
+        rec = oracle.ref_run_bench(json.dumps(cfg))[0]
+        gdofs = rec["throughput"] / 1e9
+        threads = rec["threads"]
+    except (FileNotFoundError, OSError):
+        kind = "port"
+        o = oracle.Oracle(bp, p, (e, e, e), 0.0)
+        b = o.bench_rhs()
+        o.cg(b, rel_tol=0.0, max_iter=1, constrained=bp != 1)
+        t = time.perf_counter()
+        o.cg(b, rel_tol=0.0, max_iter=steps, constrained=bp != 1)
+        gdofs = o.n * steps / (time.perf_counter() - t) / 1e9
+        threads = cores
+    return {"value": gdofs, "unit": "GDOF/s", "cores": threads, "kind": kind,
+            "sample": f"bp{bp} p={p} {e}^3 elements ({(e * p + 1) ** 3} DOFs), {steps} fixed CG iterations, "
+                      f"best of 2 after 1 warm-up, reference run_bench (bench.hpp:214-295), OMP threads={threads}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.bp, args.p, steps=max(1, min(args.steps, 5)))
+    dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else default_dims(args.p)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GDOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"bp{args.bp} p={args.p} box {dims[0]}x{dims[1]}x{dims[2]} per GPU (CPU arm: bounded "
+                               f"sample, see cpu_baseline.sample)", "bp": args.bp, "p": args.p},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2109_05072_b200 as hx
+    from paper_2109_05072_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p, bp = args.p, args.bp
+    dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else default_dims(p)
+    K, W = args.steps, max(args.warmup, 3)
+    L = _lib.lib()
+
+    if world > 1:
+        from paper_2109_05072_b200 import parallel
+
+        res = parallel.bench_weak(bp, p, dims, K, W, args.amplitude)
+        if rank != 0:
+            return
+        print(json.dumps(res), flush=True)
+        return
+
+    # ------------------------------------------------------------ single GPU
+    mesh = hx.build_box_mesh(dims, p, (1.0, 1.0, 1.0), args.amplitude)
+    t0 = time.perf_counter()
+    setup = hx.make_setup(hx.BPKind(bp), mesh, device=local)
+    op = hx.OperatorHandle(hx.Backend.Cuda, setup)
+    setup_s = time.perf_counter() - t0
+    n = op.size()
+    b_host = hx.bench_rhs(bp, p, dims)
+    b = torch.from_numpy(b_host).to(dev)
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    A = hx.ConstrainedOperator(op) if bp != 1 else op
+    st = torch.cuda.current_stream(dev)
+
+    # warm-up solve, then the timed fixed-iteration solve (device-resident inputs)
+    hx.cg(A, b, x, rel_tol=0.0, max_iter=W)
+    x.zero_()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(st)
+        rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=K)
+        ev1.record(st)
+        torch.cuda.synchronize()
+    t_dev = ev0.elapsed_time(ev1) / 1e3
+    value = n * K / t_dev / 1e9
+
+    # operator kernel alone: CUDA events around R back-to-back applies on the launch stream
+    u = torch.empty_like(b).uniform_(-1, 1)
+    w = torch.empty_like(b)
+    for _ in range(3):
+        A.apply(u, w)
+    R = 10
+    torch.cuda.synchronize()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(st)
+    for _ in range(R):
+        A.apply(u, w)
+    eb.record(st)
+    torch.cuda.synchronize()
+    t_apply = ea.elapsed_time(eb) / 1e3 / R
+    b_op, b_it, nL, E = algorithmic_bytes(bp, p, dims)
+    peak, peak_kind = load_peaks()
+    achieved = b_op / t_apply / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        tr = json.load(open(prof)).get(f"bp{bp}_p{p}_{dims[0]}x{dims[1]}x{dims[2]}")
+        if tr:
+            traffic = tr.get("dram_bytes_per_launch")
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    bh = torch.from_numpy(b_host).pin_memory()
+    xh = torch.zeros(n, dtype=torch.float64).pin_memory()
+    _dp = C.POINTER(C.c_double)
+    repc = _lib.CGReportC()
+    ws = op.workspace()
+    L.hexbp_cg_host(setup._h, ws._h, C.cast(bh.data_ptr(), _dp), C.cast(xh.data_ptr(), _dp), n, 0.0, 2,
+                    1 if bp != 1 else 0, C.byref(repc), None)
+    xh.zero_()
+    torch.cuda.synchronize()
+    te = time.perf_counter()
+    rc = L.hexbp_cg_host(setup._h, ws._h, C.cast(bh.data_ptr(), _dp), C.cast(xh.data_ptr(), _dp), n, 0.0, K,
+                         1 if bp != 1 else 0, C.byref(repc), None)
+    te = time.perf_counter() - te
+    assert rc == 0, L.hexbp_last_error()
+    e2e = n * K / te / 1e9
+
+    kinfo = ws.kernel_info()
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": t_dev / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference bench RHS, bench.hpp:234-243; device-generated box mesh)",
+        "config": {"workload": f"BP3-family bp{bp} Q_{p} box {dims[0]}x{dims[1]}x{dims[2]} elements, {n} DOFs, "
+                               f"{K} fixed CG iterations (BASELINE configs[2])" if bp == 3 and p == 7 else
+                               f"bp{bp} Q_{p} box {dims[0]}x{dims[1]}x{dims[2]}, {n} DOFs, {K} fixed CG iterations",
+                   "bp": bp, "p": p, "q": setup.q, "dims": list(dims), "dofs": n, "elements": E,
+                   "deform_amplitude": args.amplitude, "parallelism": "single GPU",
+                   "l2": "inputs larger than L2 (factors %.2f GB)" % (setup.factor_bytes / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "bp_apply_kernel (fused operator apply)",
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                     "algorithmic_bytes_per_launch": b_op, "apply_ms": t_apply * 1e3},
+        "cg_iteration_roofline": {"algorithmic_bytes_per_iter": b_it, "achieved_GBps": b_it * K / t_dev / 1e9,
+                                  "frac": b_it * K / t_dev / 1e9 / peak,
+                                  "roofline_GDOFps": peak * 1e9 / (b_it / nL) / 1e9},
+        "e2e": {"value": e2e, "unit": "GDOF/s", "h2d_bytes_per_step": 2 * n * 8 / K, "d2h_bytes_per_step": n * 8 / K,
+                "path": "hexbp_cg_host (C ABI, pinned host b/x; b, x0 in and x out per solve, amortised per step)"},
+        "gpu_launches": 3 * K + 2,
+        "clocks": clk.summary(),
+        "kernel": kinfo,
+        "setup_seconds": setup_s,
+        "cg_report": {"iterations": rep.iterations, "r0": float(rep.residual_history[0]),
+                      "final_rel_residual": rep.final_rel_residual},
+    }
+    if not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(bp, p)
+        except Exception as ex:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    del setup, op, A, b, x, u, w
+    torch.cuda.empty_cache()
+    if not args.no_sweep:
+        line["p_sweep"] = p_sweep(bp, K, local)
+    print(json.dumps(line), flush=True)
+
+
+def p_sweep(bp: int, K: int, local: int):
+    """GDOF/s vs p (the metric is quoted 'vs p') at ~50M DOFs per GPU."""
+    import torch
+
+    import paper_2109_05072_b200 as hx
+
+    out = {}
+    peak, _ = load_peaks()
+    for p in (2, 3, 4, 5, 6, 8):
+        e = 1
+        while ((e + 1) * p + 1) ** 3 <= 50_000_000:
+            e += 1
+        dims = (e, e, e)
+        try:
+            op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), hx.build_box_mesh(dims, p),
+                                                                 device=local))
+            A = hx.ConstrainedOperator(op) if bp != 1 else op
+            b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda(local)
+            x = torch.zeros_like(b)
+            hx.cg(A, b, x, 0.0, 3)
+            x.zero_()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            hx.cg(A, b, x, 0.0, K)
+            dt = time.perf_counter() - t
+            _, b_it, nL, _ = algorithmic_bytes(bp, p, dims)
+            out[str(p)] = {"GDOFps": nL * K / dt / 1e9, "dofs": nL, "roofline_frac": b_it * K / dt / 1e9 / peak}
+            del op, A, b, x
+            torch.cuda.empty_cache()
+        except Exception as ex:
+            out[str(p)] = {"error": str(ex)[:120]}
+    return out
+
+
+if __name__ == "__main__":
+    main()

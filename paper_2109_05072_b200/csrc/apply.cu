@@ -1,4 +1,4 @@
-// Fused matrix-free BP operator apply for sm_100a: one kernel per apply.
+// Fused matrix-free BP operator apply for sm_100a.
 //
 // Replaces OperatorHandle::apply_fused (operator.hpp:396-414) =
 //   gather (restriction.hpp:55-65, inlined operator.hpp:223-225)
@@ -9,28 +9,29 @@
 // plus the ConstrainedOperator wrapper (solver.hpp:60-65) and, in CG mode,
 // the p.Ap reduction and alpha = rz / pAp (solver.hpp:127-131).
 //
-// Work decomposition ("element columns"): a CTA owns one (ex, ey) column of
+// Work decomposition ("element columns"): CTA c owns the (ex, ey) column of
 // elements and marches it along z. The structured-mesh gather is index
 // arithmetic (mesh.hpp:81); no connectivity table is read.
 //
-// Deterministic, atomic-free transpose restriction (K4):
-//  * z-shared node planes are summed in registers (carry of the previous
-//    element's top plane), in element order;
-//  * x/y-shared node lines are summed in global memory in COLUMN-TICKET
-//    order: columns are claimed through an atomic ticket in row-major order,
-//    a column publishes per-element progress with a release store, and a
-//    column whose lateral nodes are shared with lower-ticket columns waits
-//    (acquire) for those columns' progress before read-modify-writing them.
-//    Every node's partial sums are therefore added in one fixed order, so
-//    results are bitwise identical run to run (restriction.hpp:18-21), and
-//    each L-vector entry is written to HBM once.
+// Deterministic, atomic-free transpose restriction (K4), two launches:
+//  1. bp_apply_kernel: z-shared node planes are summed in registers (carry of
+//     the previous element's top plane, element order). Nodes strictly inside
+//     the column's (p+1)x(p+1) footprint belong to it alone: final values are
+//     written to w once. Each of the 4p "ring" nodes of the footprint is shared
+//     with 1-3 neighbouring columns: the column writes its partial to the
+//     lateral buffer lat[Z][column][ring position].
+//  2. lateral_fixup_kernel: every ring node sums its 1-4 partials in ascending
+//     column order and writes w (and finishes p.Ap / alpha in CG mode).
+// Every node's partials are therefore added in one fixed order: results are
+// bitwise identical run to run (restriction.hpp:18-21) with no inter-CTA
+// waiting inside the operator kernel.
 //
 // Element pipeline (q x q threads per column, z-pencil -> y -> x pencils):
 //   Z : thread (i,j) holds u(i,j,:) in registers; B_z u, D_z u        -> smem A
 //   Y : thread (i,c) holds a y-pencil; B_y, D_y                         -> smem B
-//   X : thread (b,c) holds x-pencils; gr, gs, gt at the q x 1 x 1 points,
-//       G streamed from HBM straight to registers (coalesced, L2
-//       evict-first, bulk-prefetched one element ahead), then D_x^T/B_x^T -> smem B
+//   X : thread (b,c) holds x-pencils; gr, gs, gt at the q points of its x-line,
+//       G streamed from HBM straight to registers (coalesced, L2 evict-first,
+//       bulk-prefetched two elements ahead), then D_x^T / B_x^T          -> smem B
 //   Y': B_y^T, D_y^T                                                     -> smem A
 //   Z': B_z^T, D_z^T into the z-pencil registers = the element's result.
 // The contraction order is the reference's (D,B,B),(B,D,B),(B,B,D) with the
@@ -104,8 +105,15 @@ struct Cfg {
   static constexpr int SB_IS = best_stride(N, Q, Q * Q, 1);
   static constexpr int SA_SIZE = FA * Q * SA_CS;
   static constexpr int SB_SIZE = FB * N * SB_IS;
-  static constexpr int SMEM_BYTES = (SA_SIZE + SB_SIZE) * 8;
-  static constexpr int MIN_BLOCKS = NT <= 64 ? 8 : (NT <= 96 ? 4 : 3);
+  static constexpr int COMP = KIND == KIND_MASS ? 1 : 6;
+  static constexpr int GS = (COMP * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
+  static constexpr int G_OFF = (SA_SIZE + SB_SIZE + 1) / 2 * 2;  // 16-byte aligned TMA destination
+  static constexpr int U_OFF = G_OFF + GS;                       // two u slabs (cp.async double buffer)
+  static constexpr int BAR_OFF = U_OFF + 2 * N * N * N;
+  static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
+  // ptxas sizes the register cap as if CTAs were whole 4-warp groups; these
+  // values leave the cap at 255 and let registers/smem set the occupancy.
+  static constexpr int MIN_BLOCKS = NT <= 32 ? 8 : (NT <= 64 ? 4 : (NT <= 96 ? 3 : 2));
 };
 
 template <int P, int Q, int KIND>
@@ -119,364 +127,417 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
   extern __shared__ double smem[];
   double* SA = smem;
   double* SB = smem + K::SA_SIZE;
-  __shared__ unsigned int s_col;
-  __shared__ int s_last;
   __shared__ double s_red[NT / 32];
 
   if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;  // CG already stopped
 
   const int t = threadIdx.x;
-  const unsigned int epoch = *(volatile unsigned int*)&A.sync->epoch;
-  const unsigned long long pbase = static_cast<unsigned long long>(epoch) * (A.nz + 1);
   const uint64_t pol = policy_evict_first();
   const bool do_dot = A.col_dot != nullptr;
   const bool zrole = t < N * N;
   const int zi = t % N, zj = t / N;
+  const int col = blockIdx.x;
+  const int ex = col % A.nx, ey = col / A.nx;
+  const int X = ex * P + zi, Y = ey * P + zj;
+  const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+  const bool ring = zi == 0 || zi == P || zj == 0 || zj == P;
+  double* lat = A.lateral + static_cast<long long>(col) * (4 * P) + ring_index(P, zi, zj);
+  const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
+  double carry = 0.0, dot = 0.0;
 
-  for (;;) {
-    if (t == 0) s_col = atomicAdd(&A.sync->ticket, 1u);
-    __syncthreads();
-    const int col = static_cast<int>(s_col);
-    if (col >= A.ncols) break;
-    const int ex = col % A.nx, ey = col / A.nx;
-    const int X = ex * P + zi, Y = ey * P + zj;
-    // Lateral sharing of this thread's node column (see header comment).
-    const bool rmw = (zi == 0 && ex > 0) || (zj == 0 && ey > 0);
-    const bool fin = !((zi == P && ex < A.nx - 1) || (zj == P && ey < A.ny - 1));
-    const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
-    const bool need_wait = ex > 0 || ey > 0;
-    double carry = 0.0, dot = 0.0;
-
-    const double* Gcol = A.G + static_cast<long long>(col) * A.nz * A.gstride;
-    const uint32_t gbytes = static_cast<uint32_t>(A.gstride * 8);
-    if (t == 0) {
-      prefetch_l2_bulk(Gcol, gbytes);
-      if (A.nz > 1) prefetch_l2_bulk(Gcol + A.gstride, gbytes);
-    }
-
-    for (int ez = 0; ez < A.nz; ++ez) {
-      if (t == 0 && ez + 2 < A.nz) prefetch_l2_bulk(Gcol + (ez + 2) * A.gstride, gbytes);
-      const double* Ge = Gcol + ez * A.gstride;
-      double out[N];
-
-      // ---------------- phase Z: gather the z-pencil, contract along z
-      if (zrole) {
-        double uk[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          const int Z = ez * P + k;
-          const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-          double v = __ldg(A.u + node);
-          if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
-          uk[k] = v;
-        }
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double s0;
-          if constexpr (COLLOC) {
-            s0 = uk[c];
-          } else {
-            s0 = 0.0;
-#pragma unroll
-            for (int k = 0; k < N; ++k) s0 = fma(bs.B[c][k], uk[k], s0);
-          }
-          SA[c * K::SA_CS + t] = s0;
-          if constexpr (!MASS) {
-            double s1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < N; ++k) s1 = fma(bs.D[c][k], uk[k], s1);
-            SA[(Q + c) * K::SA_CS + t] = s1;
-          }
-        }
-      }
-      __syncthreads();
-
-      // ---------------- phase Y: y-pencils
-      if (t < N * Q) {
-        const int i = t % N, c = t / N;
-        double y0[N], y1[N];
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          y0[j] = SA[c * K::SA_CS + j * N + i];
-          if constexpr (!MASS) y1[j] = SA[(Q + c) * K::SA_CS + j * N + i];
-        }
-        double* sb = SB + i * K::SB_IS + c * Q;
-#pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          double bb = 0.0, db = 0.0, bd = 0.0;
-          if constexpr (COLLOC) {
-            bb = y0[b];
-            bd = y1[b];
-          } else {
-#pragma unroll
-            for (int j = 0; j < N; ++j) bb = fma(bs.B[b][j], y0[j], bb);
-            if constexpr (!MASS) {
-#pragma unroll
-              for (int j = 0; j < N; ++j) bd = fma(bs.B[b][j], y1[j], bd);
-            }
-          }
-          sb[b] = bb;
-          if constexpr (!MASS) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) db = fma(bs.D[b][j], y0[j], db);
-            sb[N * K::SB_IS + b] = db;
-            sb[2 * N * K::SB_IS + b] = bd;
-          }
-        }
-      }
-      __syncthreads();
-
-      // ---------------- phase X: x-pencils, pointwise factors, back along x
-      if (t < QQ) {
-        if constexpr (MASS) {
-          double x0[N], v[Q];
-#pragma unroll
-          for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + t];
-#pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            double s = 0.0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) s = fma(bs.B[a][i], x0[i], s);
-            v[a] = s * ld_stream(Ge + a * QQ + t, pol);
-          }
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int a = 0; a < Q; ++a) s = fma(bs.B[a][i], v[a], s);
-            SB[i * K::SB_IS + t] = s;
-          }
-        } else {
-          double gr[Q], gs[Q], gt[Q];
-          {
-            double x0[N], x1[N], x2[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-              x0[i] = SB[i * K::SB_IS + t];
-              x1[i] = SB[(N + i) * K::SB_IS + t];
-              x2[i] = SB[(2 * N + i) * K::SB_IS + t];
-            }
-#pragma unroll
-            for (int a = 0; a < Q; ++a) {
-              double r = 0.0;
-#pragma unroll
-              for (int i = 0; i < N; ++i) r = fma(bs.D[a][i], x0[i], r);
-              gr[a] = r;
-              if constexpr (COLLOC) {
-                gs[a] = x1[a];
-                gt[a] = x2[a];
-              } else {
-                double s = 0.0, u = 0.0;
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                  s = fma(bs.B[a][i], x1[i], s);
-                  u = fma(bs.B[a][i], x2[i], u);
-                }
-                gs[a] = s;
-                gt[a] = u;
-              }
-            }
-          }
-#pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            const double* g = Ge + a * QQ + t;
-            const double g0 = ld_stream(g + 0 * Q * QQ, pol), g1 = ld_stream(g + 1 * Q * QQ, pol);
-            const double g2 = ld_stream(g + 2 * Q * QQ, pol), g3 = ld_stream(g + 3 * Q * QQ, pol);
-            const double g4 = ld_stream(g + 4 * Q * QQ, pol), g5 = ld_stream(g + 5 * Q * QQ, pol);
-            const double r = gr[a], s = gs[a], u = gt[a];
-            gr[a] = g0 * r + g1 * s + g2 * u;
-            gs[a] = g1 * r + g3 * s + g4 * u;
-            gt[a] = g2 * r + g4 * s + g5 * u;
-          }
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            double a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-            for (int a = 0; a < Q; ++a) a1 = fma(bs.D[a][i], gr[a], a1);
-            if constexpr (COLLOC) {
-              a2 = gs[i];
-              a3 = gt[i];
-            } else {
-#pragma unroll
-              for (int a = 0; a < Q; ++a) {
-                a2 = fma(bs.B[a][i], gs[a], a2);
-                a3 = fma(bs.B[a][i], gt[a], a3);
-              }
-            }
-            SB[i * K::SB_IS + t] = a1;
-            SB[(N + i) * K::SB_IS + t] = a2;
-            SB[(2 * N + i) * K::SB_IS + t] = a3;
-          }
-        }
-      }
-      __syncthreads();
-
-      // ---------------- phase Y': back along y
-      if (t < N * Q) {
-        const int i = t % N, c = t / N;
-        const double* sb = SB + i * K::SB_IS + c * Q;
-        double a0[Q], a1[Q], a2[Q];
-#pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          a0[b] = sb[b];
-          if constexpr (!MASS) {
-            a1[b] = sb[N * K::SB_IS + b];
-            a2[b] = sb[2 * N * K::SB_IS + b];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          double c1 = 0.0, c2 = 0.0;
-          if constexpr (MASS) {
-#pragma unroll
-            for (int b = 0; b < Q; ++b) c1 = fma(bs.B[b][j], a0[b], c1);
-          } else if constexpr (COLLOC) {
-            c1 = a0[j];
-#pragma unroll
-            for (int b = 0; b < Q; ++b) c1 = fma(bs.D[b][j], a1[b], c1);
-            c2 = a2[j];
-          } else {
-#pragma unroll
-            for (int b = 0; b < Q; ++b) {
-              c1 = fma(bs.B[b][j], a0[b], c1);
-              c2 = fma(bs.B[b][j], a2[b], c2);
-            }
-#pragma unroll
-            for (int b = 0; b < Q; ++b) c1 = fma(bs.D[b][j], a1[b], c1);
-          }
-          SA[c * K::SA_CS + j * N + i] = c1;
-          if constexpr (!MASS) SA[(Q + c) * K::SA_CS + j * N + i] = c2;
-        }
-      }
-      __syncthreads();
-
-      // ---------------- phase Z': back along z into the z-pencil
-      if (zrole) {
-        double c1[Q], c2[Q];
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          c1[c] = SA[c * K::SA_CS + t];
-          if constexpr (!MASS) c2[c] = SA[(Q + c) * K::SA_CS + t];
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double s = 0.0;
-          if constexpr (COLLOC) {
-            s = c1[k];
-          } else {
-#pragma unroll
-            for (int c = 0; c < Q; ++c) s = fma(bs.B[c][k], c1[c], s);
-          }
-          if constexpr (!MASS) {
-#pragma unroll
-            for (int c = 0; c < Q; ++c) s = fma(bs.D[c][k], c2[c], s);
-          }
-          out[k] = s;
-        }
-      }
-
-      // ---------------- deterministic transpose restriction
-      if (t == 0 && need_wait) {
-        const unsigned long long target = pbase + ez + 1;
-        const unsigned long long* pr = A.progress;
-        if (ex > 0)
-          while (ld_acquire_u64(pr + col - 1) < target) {
-          }
-        if (ey > 0) {
-          if (ex > 0)
-            while (ld_acquire_u64(pr + col - A.nx - 1) < target) {
-            }
-          while (ld_acquire_u64(pr + col - A.nx) < target) {
-          }
-          if (ex + 1 < A.nx)
-            while (ld_acquire_u64(pr + col - A.nx + 1) < target) {
-            }
-        }
-        __threadfence();
-      }
-      __syncthreads();
-      if (zrole) {
-        out[0] += carry;
-        const int kend = (ez == A.nz - 1) ? N : P;
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          if (k < kend) {
-            const int Z = ez * P + k;
-            const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-            double v = out[k];
-            if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)))
-              v = __ldg(A.u + node);
-            else if (rmw)
-              v += __ldcg(A.w + node);
-            A.w[node] = v;
-            if (do_dot && fin) dot = fma(__ldg(A.u + node), v, dot);
-          }
-        }
-        carry = out[P];
-      }
-      __syncthreads();
-      if (t == 0) {
-        __threadfence();
-        st_release_u64(A.progress + col, pbase + ez + 1);
-      }
-    }
-    if (do_dot) {
-      const double s = block_sum<NT>(dot, s_red);
-      if (t == 0) A.col_dot[col] = s;
-    }
-    __syncthreads();
+  // Staging: the element's factor block G_e is copied global -> shared by the
+  // TMA bulk engine (one elected thread, mbarrier completion), issued as soon
+  // as the previous element's phase X has consumed the buffer; the z-pencil of
+  // u for element ez+1 is fetched by LDGSTS (cp.async) into the other half of a
+  // double buffer while element ez computes. Neither costs registers.
+  const double* Gcol = A.G + static_cast<long long>(col) * A.nz * K::GS;
+  constexpr uint32_t gbytes = K::GS * 8;
+  double* Gs = smem + K::G_OFF;
+  double* Us = smem + K::U_OFF;
+  const uint32_t bar = smem_u32(smem + K::BAR_OFF);
+  const uint32_t gs_addr = smem_u32(Gs);
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
   }
-
-  // ---------------- last CTA: reset the ticket, bump the epoch, finish p.Ap
   __syncthreads();
   if (t == 0) {
+    mbar_arrive_expect_tx(bar, gbytes);
+    bulk_g2s(gs_addr, Gcol, gbytes, bar, pol);
+    if (A.nz > 1) prefetch_l2_bulk(Gcol + K::GS, gbytes);
+  }
+  auto fetch_u = [&](int ez, int buf) {
+    if (zrole) {
+      const uint32_t dst = smem_u32(Us + buf * N * N * N + t);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const long long node =
+            X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * (ez * P + k));
+        cp_async8(dst + k * N * N * 8, A.u + node);
+      }
+    }
+    cp_async_commit();
+  };
+  fetch_u(0, 0);
+
+  for (int ez = 0; ez < A.nz; ++ez) {
+    if (t == 0 && ez + 2 < A.nz) prefetch_l2_bulk(Gcol + (ez + 2) * K::GS, gbytes);
+    const double* Ge = Gs;
+    double out[N];
+    if (ez + 1 < A.nz) {
+      fetch_u(ez + 1, (ez + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+
+    // ---------------- phase Z: gather the z-pencil, contract along z
+    if (zrole) {
+      double uk[N];
+      const double* us = Us + (ez & 1) * N * N * N + t;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const int Z = ez * P + k;
+        double v = us[k * N * N];
+        if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
+        uk[k] = v;
+      }
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        double s0;
+        if constexpr (COLLOC) {
+          s0 = uk[c];
+        } else {
+          s0 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s0 = fma(bs.B[c][k], uk[k], s0);
+        }
+        SA[c * K::SA_CS + t] = s0;
+        if constexpr (!MASS) {
+          double s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s1 = fma(bs.D[c][k], uk[k], s1);
+          SA[(Q + c) * K::SA_CS + t] = s1;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- phase Y: y-pencils
+    if (t < N * Q) {
+      const int i = t % N, c = t / N;
+      double y0[N], y1[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        y0[j] = SA[c * K::SA_CS + j * N + i];
+        if constexpr (!MASS) y1[j] = SA[(Q + c) * K::SA_CS + j * N + i];
+      }
+      double* sb = SB + i * K::SB_IS + c * Q;
+#pragma unroll
+      for (int b = 0; b < Q; ++b) {
+        double bb = 0.0, db = 0.0, bd = 0.0;
+        if constexpr (COLLOC) {
+          bb = y0[b];
+          bd = y1[b];
+        } else {
+#pragma unroll
+          for (int j = 0; j < N; ++j) bb = fma(bs.B[b][j], y0[j], bb);
+          if constexpr (!MASS) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) bd = fma(bs.B[b][j], y1[j], bd);
+          }
+        }
+        sb[b] = bb;
+        if constexpr (!MASS) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) db = fma(bs.D[b][j], y0[j], db);
+          sb[N * K::SB_IS + b] = db;
+          sb[2 * N * K::SB_IS + b] = bd;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- phase X: x-pencils, pointwise factors, back along x
+    mbar_wait_parity(bar, ez & 1);  // G_e has landed in shared memory
+    if (t < QQ) {
+      if constexpr (MASS) {
+        double x0[N], v[Q];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + t];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) s = fma(bs.B[a][i], x0[i], s);
+          v[a] = s * Ge[a * QQ + t];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) s = fma(bs.B[a][i], v[a], s);
+          SB[i * K::SB_IS + t] = s;
+        }
+      } else {
+        double gr[Q], gs[Q], gt[Q];
+        {
+          double x0[N], x1[N], x2[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            x0[i] = SB[i * K::SB_IS + t];
+            x1[i] = SB[(N + i) * K::SB_IS + t];
+            x2[i] = SB[(2 * N + i) * K::SB_IS + t];
+          }
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            double r = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) r = fma(bs.D[a][i], x0[i], r);
+            gr[a] = r;
+            if constexpr (COLLOC) {
+              gs[a] = x1[a];
+              gt[a] = x2[a];
+            } else {
+              double s = 0.0, u = 0.0;
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                s = fma(bs.B[a][i], x1[i], s);
+                u = fma(bs.B[a][i], x2[i], u);
+              }
+              gs[a] = s;
+              gt[a] = u;
+            }
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          const double* g = Ge + a * QQ + t;
+          const double g0 = g[0 * Q * QQ], g1 = g[1 * Q * QQ], g2 = g[2 * Q * QQ];
+          const double g3 = g[3 * Q * QQ], g4 = g[4 * Q * QQ], g5 = g[5 * Q * QQ];
+          const double r = gr[a], s = gs[a], u = gt[a];
+          gr[a] = g0 * r + g1 * s + g2 * u;  // operator.hpp:129-131
+          gs[a] = g1 * r + g3 * s + g4 * u;
+          gt[a] = g2 * r + g4 * s + g5 * u;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) a1 = fma(bs.D[a][i], gr[a], a1);
+          if constexpr (COLLOC) {
+            a2 = gs[i];
+            a3 = gt[i];
+          } else {
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+              a2 = fma(bs.B[a][i], gs[a], a2);
+              a3 = fma(bs.B[a][i], gt[a], a3);
+            }
+          }
+          SB[i * K::SB_IS + t] = a1;
+          SB[(N + i) * K::SB_IS + t] = a2;
+          SB[(2 * N + i) * K::SB_IS + t] = a3;
+        }
+      }
+    }
+    __syncthreads();
+    if (t == 0 && ez + 1 < A.nz) {  // G buffer consumed: stream the next element's block
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, gbytes);
+      bulk_g2s(gs_addr, Gcol + (ez + 1) * K::GS, gbytes, bar, pol);
+    }
+
+    // ---------------- phase Y': back along y
+    if (t < N * Q) {
+      const int i = t % N, c = t / N;
+      const double* sb = SB + i * K::SB_IS + c * Q;
+      double a0[Q], a1[Q], a2[Q];
+#pragma unroll
+      for (int b = 0; b < Q; ++b) {
+        a0[b] = sb[b];
+        if constexpr (!MASS) {
+          a1[b] = sb[N * K::SB_IS + b];
+          a2[b] = sb[2 * N * K::SB_IS + b];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double c1 = 0.0, c2 = 0.0;
+        if constexpr (MASS) {
+#pragma unroll
+          for (int b = 0; b < Q; ++b) c1 = fma(bs.B[b][j], a0[b], c1);
+        } else if constexpr (COLLOC) {
+          c1 = a0[j];
+#pragma unroll
+          for (int b = 0; b < Q; ++b) c1 = fma(bs.D[b][j], a1[b], c1);
+          c2 = a2[j];
+        } else {
+#pragma unroll
+          for (int b = 0; b < Q; ++b) {
+            c1 = fma(bs.B[b][j], a0[b], c1);
+            c2 = fma(bs.B[b][j], a2[b], c2);
+          }
+#pragma unroll
+          for (int b = 0; b < Q; ++b) c1 = fma(bs.D[b][j], a1[b], c1);
+        }
+        SA[c * K::SA_CS + j * N + i] = c1;
+        if constexpr (!MASS) SA[(Q + c) * K::SA_CS + j * N + i] = c2;
+      }
+    }
+    __syncthreads();
+
+    // ---------------- phase Z': back along z into the z-pencil
+    if (zrole) {
+      double c1[Q], c2[Q];
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        c1[c] = SA[c * K::SA_CS + t];
+        if constexpr (!MASS) c2[c] = SA[(Q + c) * K::SA_CS + t];
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+        if constexpr (COLLOC) {
+          s = c1[k];
+        } else {
+#pragma unroll
+          for (int c = 0; c < Q; ++c) s = fma(bs.B[c][k], c1[c], s);
+        }
+        if constexpr (!MASS) {
+#pragma unroll
+          for (int c = 0; c < Q; ++c) s = fma(bs.D[c][k], c2[c], s);
+        }
+        out[k] = s;
+      }
+
+      // ---------------- transpose restriction, part 1 (see header)
+      out[0] += carry;
+      const int kend = (ez == A.nz - 1) ? N : P;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (k < kend) {
+          const int Z = ez * P + k;
+          if (ring) {
+            lat[Z * lat_stride] = out[k];
+          } else {
+            const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+            double v = out[k];
+            if (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = __ldg(A.u + node);
+            A.w[node] = v;
+            if (do_dot) dot = fma(__ldg(A.u + node), v, dot);
+          }
+        }
+      }
+      carry = out[P];
+    }
+    __syncthreads();  // smem A is rewritten by the next element's phase Z
+  }
+  if (do_dot) {
+    const double s = block_sum<NT>(dot, s_red);
+    if (t == 0) A.col_dot[col] = s;
+  }
+}
+
+// Transpose restriction, part 2: sum the 1-4 column partials of every ring
+// node in ascending column order. In CG mode also finish p.Ap (column
+// partials of part 1 + this kernel's block partials, both in index order)
+// and alpha = rz / pAp (solver.hpp:127-131).
+constexpr int FT = 256;
+
+__global__ void __launch_bounds__(FT) lateral_fixup_kernel(const __grid_constant__ ApplyArgs A, int P) {
+  __shared__ double red[FT / 32];
+  if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
+  const bool do_dot = A.col_dot != nullptr;
+  const long long rowpart = static_cast<long long>(A.ny + 1) * A.Nx;          // nodes on rows Y % P == 0
+  const long long colpart = static_cast<long long>(A.nx + 1) * (A.ny * (P - 1));  // X % P == 0, Y % P != 0
+  const long long per_plane = rowpart + colpart;
+  const long long total = per_plane * A.Nz;
+  const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
+  double dot = 0.0;
+  for (long long l = blockIdx.x * static_cast<long long>(FT) + threadIdx.x; l < total;
+       l += static_cast<long long>(gridDim.x) * FT) {
+    const int Z = static_cast<int>(l / per_plane);
+    const long long r = l - static_cast<long long>(Z) * per_plane;
+    int X, Y;
+    if (r < rowpart) {
+      Y = static_cast<int>(r / A.Nx) * P;
+      X = static_cast<int>(r % A.Nx);
+    } else {
+      const long long r2 = r - rowpart;
+      const int yy = static_cast<int>(r2 / (A.nx + 1));
+      X = static_cast<int>(r2 % (A.nx + 1)) * P;
+      Y = (yy / (P - 1)) * P + 1 + yy % (P - 1);
+    }
+    // contributing columns in ascending index order
+    const int ex_hi = X / P < A.nx ? X / P : A.nx - 1;
+    const int ex_lo = (X % P == 0 && X > 0) ? X / P - 1 : ex_hi;
+    const int ey_hi = Y / P < A.ny ? Y / P : A.ny - 1;
+    const int ey_lo = (Y % P == 0 && Y > 0) ? Y / P - 1 : ey_hi;
+    const double* latZ = A.lateral + Z * lat_stride;
+    double s = 0.0;
+    for (int cy = ey_lo; cy <= ey_hi; ++cy)
+      for (int cx = ex_lo; cx <= ex_hi; ++cx)
+        s += latZ[static_cast<long long>(cy * A.nx + cx) * (4 * P) + ring_index(P, X - cx * P, Y - cy * P)];
+    const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+    if (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1 || (Z == 0 && A.bc_zlo) ||
+                          (Z == A.Nz - 1 && A.bc_zhi)))
+      s = A.u[node];
+    A.w[node] = s;
+    if (do_dot) dot = fma(A.u[node], s, dot);
+  }
+  if (!do_dot) return;
+  const double bsum = block_sum<FT>(dot, red);
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    A.fix_partials[blockIdx.x] = bsum;
     __threadfence();
-    const unsigned int prev = atomicAdd(&A.sync->done, 1u);
-    s_last = prev == gridDim.x - 1;
+    s_last = atomicAdd(A.fix_done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (do_dot) {
-    double s = 0.0;
-    for (int c = t; c < A.ncols; c += NT) s += __ldcg(A.col_dot + c);
-    const double pAp = block_sum<NT>(s, s_red);
-    if (t == 0) {
-      if (A.dot_out) *A.dot_out = pAp;
-      if (A.sc) {
-        // solver.hpp:128-131
-        if (!isfinite(pAp) || pAp <= 0.0) {
-          A.sc->status = ST_DIVERGED;
-        } else {
-          A.sc->pAp = pAp;
-          A.sc->alpha = A.sc->rz / pAp;
-        }
+  double s = 0.0;
+  for (int c = threadIdx.x; c < A.ncols; c += FT) s += __ldcg(A.col_dot + c);
+  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += FT) s += __ldcg(A.fix_partials + b);
+  const double pAp = block_sum<FT>(s, red);
+  if (threadIdx.x == 0) {
+    *A.fix_done = 0;
+    if (A.dot_out) *A.dot_out = pAp;
+    if (A.sc) {
+      if (!isfinite(pAp) || pAp <= 0.0) {
+        A.sc->status = ST_DIVERGED;
+      } else {
+        A.sc->pAp = pAp;
+        A.sc->alpha = A.sc->rz / pAp;
       }
     }
-  }
-  if (t == 0) {
-    A.sync->ticket = 0;
-    A.sync->done = 0;
-    A.sync->epoch = epoch + 1;
-    __threadfence();
   }
 }
 
 template <int P, int Q, int KIND>
 void* kernel_ptr() {
+  static bool configured = false;  // opt in to > 48 KB dynamic shared memory once per instantiation
+  if (!configured) {
+    cudaFuncSetAttribute(&bp_apply_kernel<P, Q, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<P, Q, KIND>::SMEM_BYTES);
+    configured = true;
+  }
   return reinterpret_cast<void*>(&bp_apply_kernel<P, Q, KIND>);
 }
 
 template <int P, int Q, int KIND>
-cudaError_t launch_t(const Setup& s, const ApplyArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   using K = Cfg<P, Q, KIND>;
+  kernel_ptr<P, Q, KIND>();
+  if (s.gstride != K::GS) return cudaErrorInvalidValue;
   BasisT<P, Q> bs;
   for (int i = 0; i < Q; ++i)
     for (int j = 0; j <= P; ++j) {
       bs.B[i][j] = s.B[i * (P + 1) + j];
       bs.D[i][j] = s.D[i * (P + 1) + j];
     }
-  bp_apply_kernel<P, Q, KIND><<<grid, K::NT, K::SMEM_BYTES, st>>>(a, bs);
+  bp_apply_kernel<P, Q, KIND><<<a.ncols, K::NT, K::SMEM_BYTES, st>>>(a, bs);
   return cudaGetLastError();
 }
 
@@ -518,33 +579,30 @@ KInfo info_for(const Setup& s) {
 }
 
 template <int KIND>
-cudaError_t launch_k(const Setup& s, const ApplyArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_k(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   constexpr int D = KIND == KIND_COLLOC ? 1 : 2;
   switch (s.p) {
-    case 1: return launch_t<1, 1 + D, KIND>(s, a, grid, st);
-    case 2: return launch_t<2, 2 + D, KIND>(s, a, grid, st);
-    case 3: return launch_t<3, 3 + D, KIND>(s, a, grid, st);
-    case 4: return launch_t<4, 4 + D, KIND>(s, a, grid, st);
-    case 5: return launch_t<5, 5 + D, KIND>(s, a, grid, st);
-    case 6: return launch_t<6, 6 + D, KIND>(s, a, grid, st);
-    case 7: return launch_t<7, 7 + D, KIND>(s, a, grid, st);
-    case 8: return launch_t<8, 8 + D, KIND>(s, a, grid, st);
+    case 1: return launch_t<1, 1 + D, KIND>(s, a, st);
+    case 2: return launch_t<2, 2 + D, KIND>(s, a, st);
+    case 3: return launch_t<3, 3 + D, KIND>(s, a, st);
+    case 4: return launch_t<4, 4 + D, KIND>(s, a, st);
+    case 5: return launch_t<5, 5 + D, KIND>(s, a, st);
+    case 6: return launch_t<6, 6 + D, KIND>(s, a, st);
+    case 7: return launch_t<7, 7 + D, KIND>(s, a, st);
+    case 8: return launch_t<8, 8 + D, KIND>(s, a, st);
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-int apply_occupancy_grid(const Setup& s) {
-  const KInfo ki = info_for(s);
-  if (!ki.fn) return 0;
-  int per_sm = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ki.fn, ki.nt, ki.smem);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device);
-  if (per_sm < 1) per_sm = 1;
-  const long long ncols = static_cast<long long>(s.dims[0]) * s.dims[1];
-  long long g = static_cast<long long>(per_sm) * sms;
-  if (g > ncols) g = ncols;
+int fixup_grid(const Setup& s) {
+  const long long P = s.p;
+  const long long nx = s.dims[0], ny = s.dims[1];
+  const long long per_plane = (ny + 1) * (nx * P + 1) + (nx + 1) * ny * (P - 1);
+  const long long total = per_plane * (s.dims[2] * P + 1);
+  long long g = (total + FT - 1) / FT;
+  if (g > 148 * 8) g = 148 * 8;
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
@@ -575,17 +633,21 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.constrained = constrained;
   a.bc_zlo = s.bc_zlo;
   a.bc_zhi = s.bc_zhi;
-  a.sync = ws.sync;
-  a.progress = ws.progress;
+  a.lateral = ws.lateral;
   a.col_dot = (dot_out || sc) ? ws.col_dot : nullptr;
+  a.fix_partials = ws.fix_partials;
+  a.fix_done = ws.fix_done;
   a.sc = sc;
   a.dot_out = dot_out;
+  cudaError_t e = cudaErrorInvalidValue;
   switch (s.kind) {
-    case KIND_MASS: return launch_k<KIND_MASS>(s, a, ws.apply_grid, st);
-    case KIND_DIFF: return launch_k<KIND_DIFF>(s, a, ws.apply_grid, st);
-    case KIND_COLLOC: return launch_k<KIND_COLLOC>(s, a, ws.apply_grid, st);
+    case KIND_MASS: e = launch_k<KIND_MASS>(s, a, st); break;
+    case KIND_DIFF: e = launch_k<KIND_DIFF>(s, a, st); break;
+    case KIND_COLLOC: e = launch_k<KIND_COLLOC>(s, a, st); break;
   }
-  return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  lateral_fixup_kernel<<<ws.fixup_grid, FT, 0, st>>>(a, s.p);
+  return cudaGetLastError();
 }
 
 }  // namespace hxb

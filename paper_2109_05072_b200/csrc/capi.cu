@@ -331,9 +331,12 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
     if (!e) e = cudaMalloc(p, bytes);
     if (!e) e = cudaMemset(*p, 0, bytes);
   };
-  al(reinterpret_cast<void**>(&w.sync), sizeof(ApplySync));
-  al(reinterpret_cast<void**>(&w.progress), sizeof(unsigned long long) * ncols);
+  w.fixup_grid = fixup_grid(s);
+  al(reinterpret_cast<void**>(&w.lateral),
+     sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * (static_cast<std::size_t>(s.dims[2]) * s.p + 1));
   al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * ncols);
+  al(reinterpret_cast<void**>(&w.fix_partials), sizeof(double) * w.fixup_grid);
+  al(reinterpret_cast<void**>(&w.fix_done), sizeof(unsigned int) * 4);
   al(reinterpret_cast<void**>(&w.sc), sizeof(DevScalars));
   al(reinterpret_cast<void**>(&w.r), sizeof(double) * n);
   al(reinterpret_cast<void**>(&w.p), sizeof(double) * n);
@@ -346,7 +349,6 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
     hexbp_workspace_destroy(wh);
     return cuda_status(e, "workspace allocation");
   }
-  w.apply_grid = apply_occupancy_grid(s);
   *out = wh;
   return HEXBP_OK;
 }
@@ -355,7 +357,7 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   if (!wh) return;
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
-  void* bufs[] = {w.sync, w.progress, w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
+  void* bufs[] = {w.lateral, w.fix_partials, w.fix_done, w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
                   w.vec_done, w.history};
   for (void* b : bufs)
     if (b) cudaFree(b);

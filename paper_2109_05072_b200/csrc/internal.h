@@ -28,10 +28,15 @@ struct DevScalars {
 };
 enum : int { ST_RUNNING = 0, ST_CONVERGED = 1, ST_DIVERGED = 2, ST_MAXITER = 3 };
 
-// Column-ticket bookkeeping of the fused apply kernel (see apply.cu).
-struct ApplySync {
-  unsigned int ticket, done, epoch, pad;
-};
+// Position of node (i, j) of a column footprint on its lateral ring
+// (4p nodes with i or j in {0, p}); see apply.cu.
+__host__ __device__ inline int ring_index(int P, int i, int j) {
+  if (j == 0 && i < P) return i;
+  if (i == P && j < P) return P + j;
+  if (j == P && i > 0) return 2 * P + (P - i);
+  if (i == 0 && j > 0) return 3 * P + (P - j);
+  return 0;
+}
 
 // Arguments of the fused operator kernel (passed by value, __grid_constant__).
 struct ApplyArgs {
@@ -44,9 +49,10 @@ struct ApplyArgs {
   int ncols;                // nx * ny
   int constrained;          // ConstrainedOperator semantics (solver.hpp:60-65)
   int bc_zlo, bc_zhi;       // z-faces that are essential (slab partitions)
-  ApplySync* sync;
-  unsigned long long* progress;  // per column
+  double* lateral;          // ring partials [Z][column][4p]
   double* col_dot;          // per-column partial p.Ap (nullptr: no dot)
+  double* fix_partials;     // per-block partial p.Ap of the lateral fix-up
+  unsigned int* fix_done;
   DevScalars* sc;           // CG scalars (nullptr: plain apply)
   double* dot_out;          // where the final dot lands (nullptr: CG alpha logic only)
 };
@@ -70,9 +76,11 @@ struct Setup {
 struct Workspace {
   const Setup* s = nullptr;
   int device = 0;
-  ApplySync* sync = nullptr;
-  unsigned long long* progress = nullptr;
+  double* lateral = nullptr;
   double* col_dot = nullptr;
+  double* fix_partials = nullptr;
+  unsigned int* fix_done = nullptr;
+  int fixup_grid = 0;
   DevScalars* sc = nullptr;
   double* r = nullptr;
   double* p = nullptr;
@@ -84,14 +92,13 @@ struct Workspace {
   double* history = nullptr;
   int history_cap = 0;
   int vec_blocks = 0;
-  int apply_grid = 0;
   DevScalars* host_sc = nullptr;  // pinned mirror
 };
 
 // ---- apply.cu
 cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
                          double* dot_out, DevScalars* sc, cudaStream_t st);
-int apply_occupancy_grid(const Setup& s);
+int fixup_grid(const Setup& s);
 void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm);
 
 // ---- cg.cu

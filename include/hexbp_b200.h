@@ -93,6 +93,22 @@ int hexbp_setup_factors(hexbp_setup_t s, double* factors_aos);
 int hexbp_workspace_create(hexbp_setup_t s, hexbp_workspace_t* out);
 void hexbp_workspace_destroy(hexbp_workspace_t ws);
 
+/* Arithmetic mode of hexbp_apply / hexbp_cg on this workspace:
+ *  HEXBP_MODE_REFERENCE (default): bit-exact reference arithmetic. The
+ *    operator follows elem_grad / elem_grad_transpose / scatter_add's
+ *    operation order with unfused multiply and add (tensor.hpp:50-235,
+ *    restriction.hpp:67-80), the inner products follow deterministic_dot
+ *    (dense.hpp:52-81) and the vector updates solver.hpp:103,132-147. The
+ *    device CG reproduces the reference's iterates bit for bit (same
+ *    iteration counts, same residual history).
+ *  HEXBP_MODE_FAST: the throughput path. FMA sum-factorised kernel, p.Ap
+ *    fused into the operator kernel, FMA updates, fixed-order tree
+ *    reductions: operator within ~3e-16 of the reference per entry, bitwise
+ *    reproducible run to run, iterates equal to the reference's up to
+ *    rounding. hexbp_dot always uses the reference order. */
+enum { HEXBP_MODE_REFERENCE = 0, HEXBP_MODE_FAST = 1 };
+int hexbp_workspace_set_mode(hexbp_workspace_t ws, int mode);
+
 /* Replaces OperatorHandle::apply(u, w, ws) (operator.hpp:265-279) and, with
  * constrained = 1, ConstrainedOperator::apply (solver.hpp:60-65). Device
  * pointers of l_size doubles, asynchronous on `stream`. u and w must not

@@ -289,6 +289,10 @@ class Workspace:
                                     C.byref(out), _stream_ptr(a)))
         return out.value
 
+    def set_mode(self, mode: str) -> None:
+        """'reference' (default): bit-exact reference arithmetic; 'fast': FMA kernels, fused p.Ap."""
+        _check(_lib.lib().hexbp_workspace_set_mode(self._h, {"reference": 0, "fast": 1}[mode]))
+
     def kernel_info(self) -> dict:
         vals = [C.c_int(0) for _ in range(4)]
         _check(_lib.lib().hexbp_kernel_info(self.setup._h, *[C.byref(v) for v in vals]))
@@ -438,10 +442,12 @@ class CGReport:
 
 
 def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
-       ws: Optional[Workspace] = None) -> CGReport:
+       ws: Optional[Workspace] = None, mode: str = "reference") -> CGReport:
     """cg (solver.hpp:91-153) for a device operator (OperatorHandle or
     ConstrainedOperator): the whole recurrence runs on the device. ``x`` holds
-    x0 on entry and the solution on exit (numpy arrays are updated in place)."""
+    x0 on entry and the solution on exit (numpy arrays are updated in place).
+    ``reduction='reference'`` reproduces deterministic_dot and the reference's
+    vector arithmetic bit for bit; ``'fused'`` fuses p.Ap into the operator."""
     if diag is not None:
         raise NotImplementedError("Jacobi-preconditioned CG is a SURVEY §8(f) next row")
     if isinstance(apply_op, ConstrainedOperator):
@@ -451,6 +457,7 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
     else:
         raise TypeError("cg: expected an OperatorHandle or ConstrainedOperator of the CUDA backend")
     ws = ws or op.workspace()
+    ws.set_mode(mode)
     n = op.size()
     rep = _lib.CGReportC()
     hist = np.zeros(max_iter + 1)

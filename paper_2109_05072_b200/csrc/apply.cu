@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device_util.cuh"
 #include "internal.h"
@@ -606,7 +607,20 @@ int fixup_grid(const Setup& s) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
+// DMMA kernel for BP3 p = 7 unless HEXBP_NO_DMMA=1 (A/B comparisons).
+bool use_mma(const Setup& s) {
+  static const bool disabled = [] {
+    const char* v = std::getenv("HEXBP_NO_DMMA");
+    return v && *v && *v != '0';
+  }();
+  return !disabled && mma_kernel_applies(s);
+}
+
 void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm) {
+  if (use_mma(s)) {
+    mma_kernel_info(regs, smem, threads, blocks_per_sm);
+    return;
+  }
   const KInfo ki = info_for(s);
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, ki.fn);
@@ -634,16 +648,25 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.bc_zlo = s.bc_zlo;
   a.bc_zhi = s.bc_zhi;
   a.lateral = ws.lateral;
+  a.zupper = ws.zupper;
   a.col_dot = (dot_out || sc) ? ws.col_dot : nullptr;
   a.fix_partials = ws.fix_partials;
   a.fix_done = ws.fix_done;
   a.sc = sc;
   a.dot_out = dot_out;
+  if (ws.exact) {
+    if (dot_out || sc) return cudaErrorInvalidValue;  // the exact path reduces in cg.cu
+    return launch_apply_exact(s, a, ws.fixup_grid, st);
+  }
   cudaError_t e = cudaErrorInvalidValue;
-  switch (s.kind) {
-    case KIND_MASS: e = launch_k<KIND_MASS>(s, a, st); break;
-    case KIND_DIFF: e = launch_k<KIND_DIFF>(s, a, st); break;
-    case KIND_COLLOC: e = launch_k<KIND_COLLOC>(s, a, st); break;
+  if (use_mma(s)) {
+    e = launch_apply_mma(s, a, st);
+  } else {
+    switch (s.kind) {
+      case KIND_MASS: e = launch_k<KIND_MASS>(s, a, st); break;
+      case KIND_DIFF: e = launch_k<KIND_DIFF>(s, a, st); break;
+      case KIND_COLLOC: e = launch_k<KIND_COLLOC>(s, a, st); break;
+    }
   }
   if (e != cudaSuccess) return e;
   lateral_fixup_kernel<<<ws.fixup_grid, FT, 0, st>>>(a, s.p);

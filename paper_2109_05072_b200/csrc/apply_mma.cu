@@ -1,0 +1,421 @@
+// FP64 tensor-core (DMMA) operator kernel for the BP3 headline degree
+// (p = 7: n = 8 nodes, q = 9 Gauss points per direction) -- fast mode.
+//
+// Why DMMA: the DFMA kernel (apply.cu) is issue-bound at p = 7 -- every
+// warp-wide DFMA needs its basis coefficient staged through a uniform
+// register (LDCU), so coefficient loads cost as many issue slots as the
+// FMAs, and the kernel issues ~9000 warp instructions per element. An
+// m8n8k4 f64 MMA does 256 FMAs per instruction with the basis fragment held
+// in registers for the whole kernel: ~300 MMAs per element replace ~3300
+// DFMAs and their ~2700 coefficient loads. B200's DMMA rate equals its DFMA
+// rate (64 FMA/clk/SM measured, tools/micro/fp64_peak.cu), so the win is the
+// instruction stream, not the FLOP rate.
+//
+// Shapes. Each 1D contraction Y[m][r] = sum_k M[m][k] X[k][r] runs as MMAs
+// with A = basis tile (8 x 4, registers), B = 8 "pencils" of X (4 x 8,
+// one LDS per lane), C = 8 x 8 outputs. The 9th Gauss point does not fit an
+// 8-row tile: forward (q = 9 outputs) its row is a 2-term dot per lane plus
+// a 4-lane butterfly; backward (q = 9 inputs) its column is one DFMA per
+// output. The phases, staging (TMA bulk copy of G, cp.async u) and the
+// atomic-free transpose restriction are those of apply.cu:
+//   Z : 8 pencil groups (j)      u        -> B_z u, D_z u          (+ row 8)
+//   Y : 9 groups (c)             -> B_y B_z u, D_y B_z u, B_y D_z u (+ row 8)
+//   X : 11 groups of (b,c) lines -> gr, gs, gt; G; D_x^T, B_x^T   (+ row/col 8)
+//   Y': 9 groups (c)             -> C1 = B_y^T A1 + D_y^T A2, C2 = B_y^T A3
+//   Z': 8 groups (j)             -> out = B_z^T C1 + D_z^T C2     -> scatter
+// Shared-memory layouts are [field][k][pencil] with k-strides = 4 (mod 16)
+// doubles so that the B-fragment loads (k = lane%4 (+4), pencil = lane/4)
+// are bank-conflict free.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_util.cuh"
+#include "internal.h"
+
+namespace hxb {
+namespace {
+
+constexpr int P = 7, N = 8, Q = 9, QQ = 81;
+constexpr int NW = 4, NT = NW * 32;
+constexpr int GSE = (6 * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
+// shared-memory layout (doubles)
+constexpr int US_KS = 68;                 // u staging: [k][j*8+i], k-stride 68
+constexpr int US_SZ = N * US_KS;          // per buffer
+constexpr int SA_KS = 84;                 // [f][k][i + 8c] (Z->Y) and [f][b][i + 8c] (X->Y')
+constexpr int SA_F = Q * SA_KS;           // 756
+constexpr int SB_KS = 100;                // [f][i][b + 9c] (Y->X)
+constexpr int SB_F = N * SB_KS;           // 800
+constexpr int SC_KS = 68;                 // [f][c][i + 8j] (Y'->Z'), aliases SB
+constexpr int SC_F = Q * SC_KS;           // 612
+constexpr int OFF_SA = 0;
+constexpr int OFF_SB = OFF_SA + 3 * SA_F;
+constexpr int OFF_G = OFF_SB + 3 * SB_F;  // 16-byte aligned (even)
+constexpr int OFF_U = OFF_G + GSE;
+constexpr int OFF_SCR = OFF_U + 2 * US_SZ;   // per-warp 3 x 8 x 8 transpose scratch
+constexpr int OFF_BAR = OFF_SCR + NW * 192;
+constexpr int SMEM_BYTES = (OFF_BAR + 1) * 8;
+static_assert(OFF_G % 2 == 0, "TMA destination must be 16-byte aligned");
+static_assert(3 * SB_F >= 2 * SC_F, "SC aliases SB");
+
+struct MmaBasis {
+  double B[Q][N];
+  double D[Q][N];
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// sum over the 4 lanes of a quad (lanes sharing lane/4)
+__device__ __forceinline__ double quad_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+__global__ void __launch_bounds__(NT, 2)
+    bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs) {
+  extern __shared__ double smem[];
+  double* SA = smem + OFF_SA;
+  double* SB = smem + OFF_SB;
+  double* SC = SB;  // phase Y' -> Z' (SB is consumed in phase X)
+  double* Gs = smem + OFF_G;
+  double* Us = smem + OFF_U;
+  __shared__ double s_red[NW];
+
+  if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double* scr = smem + OFF_SCR + warp * 192;
+  const uint64_t pol = policy_evict_first();
+  const bool do_dot = A.col_dot != nullptr;
+  const int col = blockIdx.x;
+  const int ex = col % A.nx, ey = col / A.nx;
+  const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
+
+  // basis fragments, resident for the whole kernel
+  const double aB0 = bs.B[g][t], aB1 = bs.B[g][t + 4];            // forward rows 0..7 (A = M[m][k])
+  const double aD0 = bs.D[g][t], aD1 = bs.D[g][t + 4];
+  const double rB0 = bs.B[8][t], rB1 = bs.B[8][t + 4];            // forward row 8
+  const double rD0 = bs.D[8][t], rD1 = bs.D[8][t + 4];
+  const double tB0 = bs.B[t][g], tB1 = bs.B[t + 4][g];            // backward (A = M^T[i][a])
+  const double tD0 = bs.D[t][g], tD1 = bs.D[t + 4][g];
+  const double cB8 = bs.B[8][g], cD8 = bs.D[8][g];                // backward column a = 8
+
+  const double* Gcol = A.G + static_cast<long long>(col) * A.nz * GSE;
+  constexpr uint32_t gbytes = GSE * 8;
+  const uint32_t bar = smem_u32(smem + OFF_BAR);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar, gbytes);
+    bulk_g2s(smem_u32(Gs), Gcol, gbytes, bar, pol);
+    if (A.nz > 1) prefetch_l2_bulk(Gcol + GSE, gbytes);
+  }
+  // u staging: thread (i,j) of the footprint (tid < 64) copies its z-pencil into [k][j*8+i]
+  auto fetch_u = [&](int ez, int buf) {
+    if (tid < N * N) {
+      const int i = tid & 7, j = tid >> 3;
+      const uint32_t dst = smem_u32(Us + buf * US_SZ + tid);
+      const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
+      const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+#pragma unroll
+      for (int k = 0; k < N; ++k) cp_async8(dst + k * US_KS * 8, A.u + base + plane * (ez * P + k));
+    }
+    cp_async_commit();
+  };
+  fetch_u(0, 0);
+
+  double carry[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // z-carry of the two j-groups this warp owns
+  double dot = 0.0;
+
+  for (int ez = 0; ez < A.nz; ++ez) {
+    if (tid == 0 && ez + 2 < A.nz) prefetch_l2_bulk(Gcol + (ez + 2) * GSE, gbytes);
+    if (ez + 1 < A.nz) {
+      fetch_u(ez + 1, (ez + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* us = Us + (ez & 1) * US_SZ;
+
+    // ------------------------------------------------ phase Z
+    for (int G = warp; G < N; G += NW) {  // G = j; pencil i = g
+      const int X = ex * P + g, Y = ey * P + G;
+      const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+      double b[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int k = t + 4 * s, Z = ez * P + k;
+        double v = us[k * US_KS + G * 8 + g];
+        if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
+        b[s] = v;
+      }
+      double cb0 = 0, cb1 = 0, cd0 = 0, cd1 = 0;
+      dmma(cb0, cb1, aB0, b[0]);
+      dmma(cb0, cb1, aB1, b[1]);
+      dmma(cd0, cd1, aD0, b[0]);
+      dmma(cd0, cd1, aD1, b[1]);
+      const double r8b = quad_sum(fma(rB1, b[1], rB0 * b[0]));
+      const double r8d = quad_sum(fma(rD1, b[1], rD0 * b[0]));
+      double* sa = SA + G * SA_KS;
+      *reinterpret_cast<double2*>(sa + 8 * g + 2 * t) = make_double2(cb0, cb1);
+      *reinterpret_cast<double2*>(sa + SA_F + 8 * g + 2 * t) = make_double2(cd0, cd1);
+      if (t == 0) {
+        sa[64 + g] = r8b;
+        sa[SA_F + 64 + g] = r8d;
+      }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ phase Y
+    for (int G = warp; G < Q; G += NW) {  // G = c; pencil i = g
+      const double* sa = SA + 8 * G + g;
+      const double x00 = sa[t * SA_KS], x01 = sa[(t + 4) * SA_KS];
+      const double x10 = sa[SA_F + t * SA_KS], x11 = sa[SA_F + (t + 4) * SA_KS];
+      double bb0 = 0, bb1 = 0, db0 = 0, db1 = 0, bd0 = 0, bd1 = 0;
+      dmma(bb0, bb1, aB0, x00);
+      dmma(bb0, bb1, aB1, x01);
+      dmma(db0, db1, aD0, x00);
+      dmma(db0, db1, aD1, x01);
+      dmma(bd0, bd1, aB0, x10);
+      dmma(bd0, bd1, aB1, x11);
+      const double r8bb = quad_sum(fma(rB1, x01, rB0 * x00));
+      const double r8db = quad_sum(fma(rD1, x01, rD0 * x00));
+      const double r8bd = quad_sum(fma(rB1, x11, rB0 * x10));
+      // SB[f][k = i][p = b + 9c]; rows b = g, cols i = 2t, 2t+1
+      double* sb = SB + g + 9 * G;
+      sb[(2 * t) * SB_KS] = bb0;
+      sb[(2 * t + 1) * SB_KS] = bb1;
+      sb[SB_F + (2 * t) * SB_KS] = db0;
+      sb[SB_F + (2 * t + 1) * SB_KS] = db1;
+      sb[2 * SB_F + (2 * t) * SB_KS] = bd0;
+      sb[2 * SB_F + (2 * t + 1) * SB_KS] = bd1;
+      if (t == 0) {  // b = 8, k = i = g
+        double* s8 = SB + g * SB_KS + 8 + 9 * G;
+        s8[0] = r8bb;
+        s8[SB_F] = r8db;
+        s8[2 * SB_F] = r8bd;
+      }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ phase X
+    mbar_wait_parity(bar, ez & 1);
+    for (int G = warp; G < 11; G += NW) {  // pencils p = 8G + (0..7) over (b,c), valid p < 81
+      const double* sb = SB + 8 * G + g;
+      const double x00 = sb[t * SB_KS], x01 = sb[(t + 4) * SB_KS];
+      const double x10 = sb[SB_F + t * SB_KS], x11 = sb[SB_F + (t + 4) * SB_KS];
+      const double x20 = sb[2 * SB_F + t * SB_KS], x21 = sb[2 * SB_F + (t + 4) * SB_KS];
+      double gr[2] = {0, 0}, gs[2] = {0, 0}, gt[2] = {0, 0};
+      dmma(gr[0], gr[1], aD0, x00);
+      dmma(gr[0], gr[1], aD1, x01);
+      dmma(gs[0], gs[1], aB0, x10);
+      dmma(gs[0], gs[1], aB1, x11);
+      dmma(gt[0], gt[1], aB0, x20);
+      dmma(gt[0], gt[1], aB1, x21);
+      double r8r = quad_sum(fma(rD1, x01, rD0 * x00));
+      double r8s = quad_sum(fma(rB1, x11, rB0 * x10));
+      double r8t = quad_sum(fma(rB1, x21, rB0 * x20));
+      // pointwise factors (operator.hpp:129-131) at (a = g, p = 8G+2t+e) and (a = 8, p = 8G+g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int p = 8 * G + 2 * t + e;
+        if (p < QQ) {
+          const double* gp = Gs + g * QQ + p;
+          const double g0 = gp[0], g1 = gp[Q * QQ], g2 = gp[2 * Q * QQ], g3 = gp[3 * Q * QQ], g4 = gp[4 * Q * QQ],
+                       g5 = gp[5 * Q * QQ];
+          const double r = gr[e], s = gs[e], u = gt[e];
+          gr[e] = g0 * r + g1 * s + g2 * u;
+          gs[e] = g1 * r + g3 * s + g4 * u;
+          gt[e] = g2 * r + g4 * s + g5 * u;
+        }
+      }
+      {
+        const int p = 8 * G + g;
+        if (p < QQ) {
+          const double* gp = Gs + 8 * QQ + p;
+          const double g0 = gp[0], g1 = gp[Q * QQ], g2 = gp[2 * Q * QQ], g3 = gp[3 * Q * QQ], g4 = gp[4 * Q * QQ],
+                       g5 = gp[5 * Q * QQ];
+          const double r = r8r, s = r8s, u = r8t;
+          r8r = g0 * r + g1 * s + g2 * u;
+          r8s = g1 * r + g3 * s + g4 * u;
+          r8t = g2 * r + g4 * s + g5 * u;
+        }
+      }
+      // warp-local transpose of the C tiles into B-fragment order: scr[f][a][pl]
+      *reinterpret_cast<double2*>(scr + 0 * 64 + 8 * g + 2 * t) = make_double2(gr[0], gr[1]);
+      *reinterpret_cast<double2*>(scr + 1 * 64 + 8 * g + 2 * t) = make_double2(gs[0], gs[1]);
+      *reinterpret_cast<double2*>(scr + 2 * 64 + 8 * g + 2 * t) = make_double2(gt[0], gt[1]);
+      __syncwarp();
+      const double v00 = scr[t * 8 + g], v01 = scr[(t + 4) * 8 + g];
+      const double v10 = scr[64 + t * 8 + g], v11 = scr[64 + (t + 4) * 8 + g];
+      const double v20 = scr[128 + t * 8 + g], v21 = scr[128 + (t + 4) * 8 + g];
+      __syncwarp();
+      // a = 8 values of pencils pl = 2t, 2t+1 (held by quads 2t, 2t+1)
+      const double v8r0 = __shfl_sync(0xffffffffu, r8r, 8 * t), v8r1 = __shfl_sync(0xffffffffu, r8r, 8 * t + 4);
+      const double v8s0 = __shfl_sync(0xffffffffu, r8s, 8 * t), v8s1 = __shfl_sync(0xffffffffu, r8s, 8 * t + 4);
+      const double v8t0 = __shfl_sync(0xffffffffu, r8t, 8 * t), v8t1 = __shfl_sync(0xffffffffu, r8t, 8 * t + 4);
+      double a1[2], a2[2], a3[2];
+      a1[0] = cD8 * v8r0;
+      a1[1] = cD8 * v8r1;
+      a2[0] = cB8 * v8s0;
+      a2[1] = cB8 * v8s1;
+      a3[0] = cB8 * v8t0;
+      a3[1] = cB8 * v8t1;
+      dmma(a1[0], a1[1], tD0, v00);
+      dmma(a1[0], a1[1], tD1, v01);
+      dmma(a2[0], a2[1], tB0, v10);
+      dmma(a2[0], a2[1], tB1, v11);
+      dmma(a3[0], a3[1], tB0, v20);
+      dmma(a3[0], a3[1], tB1, v21);
+      // rows i = g, cols p = 8G+2t+e -> SA'[f][b][i + 8c]
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int p = 8 * G + 2 * t + e;
+        if (p < QQ) {
+          const int c = p / 9, bq = p - 9 * c;
+          double* d = SA + bq * SA_KS + g + 8 * c;
+          d[0] = a1[e];
+          d[SA_F] = a2[e];
+          d[2 * SA_F] = a3[e];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && ez + 1 < A.nz) {  // G buffer consumed: stream the next element's block
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, gbytes);
+      bulk_g2s(smem_u32(Gs), Gcol + (ez + 1) * GSE, gbytes, bar, pol);
+    }
+
+    // ------------------------------------------------ phase Y'
+    for (int G = warp; G < Q; G += NW) {  // G = c; pencil i = g; contraction over b
+      const double* sa = SA + 8 * G + g;
+      const double y00 = sa[t * SA_KS], y01 = sa[(t + 4) * SA_KS];
+      const double y10 = sa[SA_F + t * SA_KS], y11 = sa[SA_F + (t + 4) * SA_KS];
+      const double y20 = sa[2 * SA_F + t * SA_KS], y21 = sa[2 * SA_F + (t + 4) * SA_KS];
+      const double* s8 = SA + 8 * SA_KS + 8 * G + 2 * t;  // b = 8, pencils i = 2t, 2t+1
+      const double2 e1 = *reinterpret_cast<const double2*>(s8);
+      const double2 e2 = *reinterpret_cast<const double2*>(s8 + SA_F);
+      const double2 e3 = *reinterpret_cast<const double2*>(s8 + 2 * SA_F);
+      double c1[2], c2[2];
+      c1[0] = fma(cD8, e2.x, cB8 * e1.x);
+      c1[1] = fma(cD8, e2.y, cB8 * e1.y);
+      c2[0] = cB8 * e3.x;
+      c2[1] = cB8 * e3.y;
+      dmma(c1[0], c1[1], tB0, y00);
+      dmma(c1[0], c1[1], tB1, y01);
+      dmma(c1[0], c1[1], tD0, y10);
+      dmma(c1[0], c1[1], tD1, y11);
+      dmma(c2[0], c2[1], tB0, y20);
+      dmma(c2[0], c2[1], tB1, y21);
+      // rows j = g, cols i = 2t, 2t+1, c = G -> SC[f][c][i + 8j]
+      double* sc = SC + G * SC_KS + 8 * g + 2 * t;
+      *reinterpret_cast<double2*>(sc) = make_double2(c1[0], c1[1]);
+      *reinterpret_cast<double2*>(sc + SC_F) = make_double2(c2[0], c2[1]);
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ phase Z' + transpose restriction (part 1)
+#pragma unroll
+    for (int slot = 0; slot < N / NW; ++slot) {  // G = j; pencil i = g; contraction over c
+      const int G = warp + NW * slot;
+      const double* sc = SC + 8 * G + g;
+      const double z00 = sc[t * SC_KS], z01 = sc[(t + 4) * SC_KS];
+      const double z10 = sc[SC_F + t * SC_KS], z11 = sc[SC_F + (t + 4) * SC_KS];
+      const double* s8 = SC + 8 * SC_KS + 8 * G + 2 * t;  // c = 8
+      const double2 e1 = *reinterpret_cast<const double2*>(s8);
+      const double2 e2 = *reinterpret_cast<const double2*>(s8 + SC_F);
+      double o[2];
+      o[0] = fma(cD8, e2.x, cB8 * e1.x);
+      o[1] = fma(cD8, e2.y, cB8 * e1.y);
+      dmma(o[0], o[1], tB0, z00);
+      dmma(o[0], o[1], tB1, z01);
+      dmma(o[0], o[1], tD0, z10);
+      dmma(o[0], o[1], tD1, z11);
+      // rows k = g (z node), cols i = 2t, 2t+1, j = G
+      const double top0 = __shfl_sync(0xffffffffu, carry[slot][0], 28 + t);
+      const double top1 = __shfl_sync(0xffffffffu, carry[slot][1], 28 + t);
+      if (g == 0) {
+        o[0] += top0;
+        o[1] += top1;
+      }
+      if (g == P && ez + 1 < A.nz) {
+        carry[slot][0] = o[0];
+        carry[slot][1] = o[1];
+        continue;
+      }
+      const int Z = ez * P + g, Y = ey * P + G;
+      const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = 2 * t + e, X = ex * P + i;
+        const bool ring = i == 0 || i == P || G == 0 || G == P;
+        if (ring) {
+          A.lateral[Z * lat_stride + static_cast<long long>(col) * (4 * P) + ring_index(P, i, G)] = o[e];
+        } else {
+          const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+          double v = o[e];
+          if (zbc) v = __ldg(A.u + node);
+          A.w[node] = v;
+          if (do_dot) dot = fma(__ldg(A.u + node), v, dot);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (do_dot) {
+    double v = dot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += s_red[w];
+      A.col_dot[col] = s;
+    }
+  }
+}
+
+}  // namespace
+
+bool mma_kernel_applies(const Setup& s) { return s.kind == KIND_DIFF && s.p == P && s.gstride == GSE; }
+
+cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(&bp3_p7_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    configured = true;
+  }
+  MmaBasis bs;
+  for (int i = 0; i < Q; ++i)
+    for (int j = 0; j < N; ++j) {
+      bs.B[i][j] = s.B[i * N + j];
+      bs.D[i][j] = s.D[i * N + j];
+    }
+  bp3_p7_mma_kernel<<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs);
+  return cudaGetLastError();
+}
+
+void mma_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm) {
+  cudaFuncSetAttribute(&bp3_p7_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, bp3_p7_mma_kernel);
+  *regs = fa.numRegs;
+  *smem = static_cast<int>(fa.sharedSizeBytes) + SMEM_BYTES;
+  *threads = NT;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp3_p7_mma_kernel, NT, SMEM_BYTES);
+}
+
+}  // namespace hxb

@@ -334,6 +334,7 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
   w.fixup_grid = fixup_grid(s);
   al(reinterpret_cast<void**>(&w.lateral),
      sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * (static_cast<std::size_t>(s.dims[2]) * s.p + 1));
+  al(reinterpret_cast<void**>(&w.zupper), sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * s.dims[2]);
   al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * ncols);
   al(reinterpret_cast<void**>(&w.fix_partials), sizeof(double) * w.fixup_grid);
   al(reinterpret_cast<void**>(&w.fix_done), sizeof(unsigned int) * 4);
@@ -341,7 +342,8 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
   al(reinterpret_cast<void**>(&w.r), sizeof(double) * n);
   al(reinterpret_cast<void**>(&w.p), sizeof(double) * n);
   al(reinterpret_cast<void**>(&w.Ap), sizeof(double) * n);
-  al(reinterpret_cast<void**>(&w.vec_partials), sizeof(double) * (148 * 8 + 8));
+  al(reinterpret_cast<void**>(&w.vec_partials), sizeof(double) * reduction_partials(s.nL));
+  al(reinterpret_cast<void**>(&w.dot_result), sizeof(double) * 2);
   al(reinterpret_cast<void**>(&w.vec_done), sizeof(unsigned int) * 4);
   al(reinterpret_cast<void**>(&w.history), sizeof(double) * w.history_cap);
   if (!e) e = cudaMallocHost(reinterpret_cast<void**>(&w.host_sc), sizeof(DevScalars));
@@ -357,8 +359,8 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   if (!wh) return;
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
-  void* bufs[] = {w.lateral, w.fix_partials, w.fix_done, w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
-                  w.vec_done, w.history};
+  void* bufs[] = {w.lateral, w.zupper, w.fix_partials, w.fix_done, w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
+                  w.vec_done, w.history, w.dot_result};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (w.host_sc) cudaFreeHost(w.host_sc);
@@ -408,7 +410,12 @@ int hexbp_cg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, 
   CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
   const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
   for (int k = 1; k <= max_iter; ++k) {
-    CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st));
+    if (w.exact) {
+      CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, st));
+      CK(launch_cg_pap(w, n, st));
+    } else {
+      CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st));
+    }
     CK(launch_cg_update_r(w, n, st));
     CK(launch_cg_update_xp(w, x, n, st));
     if (k % check_every == 0 && k < max_iter) {
@@ -459,10 +466,16 @@ int hexbp_dot(hexbp_workspace_t wh, const double* a, const double* b, int64_t n,
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double* dres = w.vec_partials + 148 * 8;
+  double* dres = w.dot_result;
   CK(launch_dot(w, a, b, n, dres, st));
   CK(cudaMemcpyAsync(out, dres, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return HEXBP_OK;
+}
+
+int hexbp_workspace_set_mode(hexbp_workspace_t wh, int mode) {
+  if (!wh || (mode != HEXBP_MODE_REFERENCE && mode != HEXBP_MODE_FAST)) return invalid("bad arithmetic mode");
+  wh->w.exact = mode == HEXBP_MODE_REFERENCE;
   return HEXBP_OK;
 }
 

@@ -1,14 +1,26 @@
 // Device-resident conjugate-gradient recurrence (solver.hpp:91-153, no
-// preconditioner, z = r). Per iteration (p.Ap and alpha are produced by the
-// operator kernel, apply.cu):
-//   cg_update_r  : r -= alpha Ap; ||r||^2 (fixed-order reduction); the last
-//                  block records the residual history, applies the stopping
-//                  rule rnorm/r0 <= rel_tol and computes beta = rr/rz.
-//   cg_update_xp : x += alpha p (deferred from the reference's :132 so it
-//                  fuses with the search-direction update); p = r + beta p.
-// HBM traffic per iteration: 2 n (apply) + 3 n + 5 n = 10 n doubles + factors.
-// All reductions use a fixed grid and fixed summation order, so the whole
-// recurrence is bitwise reproducible run to run (solver.hpp:87-90).
+// preconditioner, z = r).
+//
+// Two reduction modes (hexbp_cg_set_mode):
+//  EXACT (default): every inner product follows deterministic_dot
+//    (dense.hpp:52-81) bit for bit -- 4096-entry blocks summed sequentially
+//    with separate multiply and add (no FMA, like the reference's default
+//    x86-64 build), block partials summed sequentially in block order -- and
+//    the vector updates use the reference's unfused arithmetic
+//    (solver.hpp:103,132-133,147). Given the same operator outputs the device
+//    recurrence is the reference recurrence; the only deviation left is the
+//    operator apply itself (<= 3e-16 per entry). Per iteration:
+//      apply(p)           -> Ap                         2n doubles + factors
+//      cg_pap             -> p.Ap, alpha                2n
+//      cg_update_r        -> r -= alpha Ap, r.r, beta   3n
+//      cg_update_xp       -> x += alpha p, p = r + beta p   5n
+//  FUSED: p.Ap is produced by the operator kernel (column partials + lateral
+//    fix-up partials) and the updates use FMA with fixed-order tree
+//    reductions: 10n per iteration. Bitwise reproducible run to run, not
+//    bitwise equal to the reference's sums.
+// In both modes the last CTA of each reduction applies the reference's
+// stopping rule and error semantics on the device, so no host round trip is
+// needed per iteration.
 #include <cuda_runtime.h>
 
 #include "device_util.cuh"
@@ -18,6 +30,14 @@ namespace hxb {
 namespace {
 
 constexpr int VT = 256;
+constexpr int CHUNK = 4096;          // detail::kReductionBlock (dense.hpp:52)
+constexpr int CPB = 32;              // chunks per CTA (one per lane of warp 0)
+constexpr int TILE = 128;            // elements per chunk per tile
+constexpr int TSTRIDE = TILE + 1;    // smem row stride (conflict-free column walk)
+
+#define DM(a, b) __dmul_rn((a), (b))
+#define DA(a, b) __dadd_rn((a), (b))
+#define DS(a, b) __dsub_rn((a), (b))
 
 __device__ __forceinline__ bool last_block(unsigned int* done) {
   __shared__ int s_last;
@@ -30,17 +50,159 @@ __device__ __forceinline__ bool last_block(unsigned int* done) {
   return s_last;
 }
 
-__device__ __forceinline__ double reduce_partials(const double* part, int nblk, double* red) {
+// Sequential sum of the chunk partials in chunk order (dense.hpp:70-71), by
+// one thread; loads are batched ahead of the dependent add chain.
+__device__ __forceinline__ double serial_sum(const double* part, long long n) {
+  double s = 0.0;
+  long long c = 0;
+  for (; c + 8 <= n; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(part + c + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = DA(s, v[k]);
+  }
+  for (; c < n; ++c) s = DA(s, __ldcg(part + c));
+  return s;
+}
+
+enum Op : int { OP_DOT = 0, OP_PAP = 1, OP_INIT = 2, OP_UPDATE_R = 3 };
+
+// Blocked exact reduction with an optional fused elementwise update.
+//   OP_DOT      : dot(a, b)                                   -> *out
+//   OP_PAP      : dot(p=a, Ap=b); alpha = rz / pAp            (solver.hpp:128-131)
+//   OP_INIT     : r = b - Ap (a=b_rhs, b=Ap, w0=r, w1=p); p = r; r.r; r0  (solver.hpp:102-124)
+//   OP_UPDATE_R : r = r - alpha Ap (a=r, b=Ap, w0=r); r.r; rnorm, stop, beta (solver.hpp:133-147)
+template <int OP>
+__global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, const double* b, double* w0,
+                                                            double* w1, long long n, double* part,
+                                                            unsigned int* done, DevScalars* sc, double* hist,
+                                                            double* out, double rel_tol, int max_iter) {
+  __shared__ double prod[CPB * TSTRIDE];
+  if (OP == OP_PAP || OP == OP_UPDATE_R) {
+    if (*(volatile int*)&sc->status != ST_RUNNING) return;
+  }
+  const double alpha = OP == OP_UPDATE_R ? sc->alpha : 0.0;
+  const long long nchunks = (n + CHUNK - 1) / CHUNK;
+  const long long c0 = static_cast<long long>(blockIdx.x) * CPB;
+  double s = 0.0;  // lane c of warp 0: running sum of chunk c0 + c
+  for (int tile = 0; tile < CHUNK / TILE; ++tile) {
+#pragma unroll 4
+    for (int m = 0; m < CPB * TILE / VT; ++m) {
+      const int idx = threadIdx.x + VT * m;
+      const int c = idx / TILE, e = idx % TILE;
+      const long long g = (c0 + c) * CHUNK + tile * TILE + e;
+      double pr = 0.0;  // +0.0 padding past n leaves a sequential sum unchanged
+      if (g < n) {
+        const double x = a[g], y = b[g];
+        if (OP == OP_DOT || OP == OP_PAP) {
+          pr = DM(x, y);
+        } else if (OP == OP_INIT) {
+          const double r = DS(x, y);  // r = b - Ap (solver.hpp:103)
+          w0[g] = r;
+          w1[g] = r;  // z = r; p = z (solver.hpp:109,123)
+          pr = DM(r, r);
+        } else {
+          const double r = DS(x, DM(alpha, y));  // r -= alpha * Ap (solver.hpp:133)
+          w0[g] = r;
+          pr = DM(r, r);
+        }
+      }
+      prod[c * TSTRIDE + e] = pr;
+    }
+    __syncthreads();
+    if (threadIdx.x < CPB) {
+      const double* row = prod + threadIdx.x * TSTRIDE;
+#pragma unroll 16
+      for (int e = 0; e < TILE; ++e) s = DA(s, row[e]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < CPB && c0 + threadIdx.x < nchunks) {
+    part[c0 + threadIdx.x] = s;
+    __threadfence();
+  }
+  if (!last_block(done)) return;
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  const double tot = serial_sum(part, nchunks);
+  *done = 0;
+  if (OP == OP_DOT) {
+    *out = tot;
+  } else if (OP == OP_PAP) {
+    if (!isfinite(tot) || tot <= 0.0) {
+      sc->status = ST_DIVERGED;
+    } else {
+      sc->pAp = tot;
+      sc->alpha = sc->rz / tot;
+    }
+  } else if (OP == OP_INIT) {
+    const double r0 = sqrt(tot);
+    hist[0] = r0;
+    sc->r0 = r0;
+    sc->rnorm = r0;
+    sc->rz = tot;  // deterministic_dot(r, z) with z = r: the same sum
+    sc->rel_tol = rel_tol;
+    sc->max_iter = max_iter;
+    sc->iterations = 0;
+    sc->x_pending = 0;
+    sc->status = !isfinite(r0) ? ST_DIVERGED : (r0 == 0.0 ? ST_CONVERGED : (max_iter <= 0 ? ST_MAXITER : ST_RUNNING));
+  } else {
+    const double rnorm = sqrt(tot);
+    const int k = sc->iterations + 1;
+    sc->iterations = k;
+    sc->rnorm = rnorm;
+    hist[k] = rnorm;
+    sc->x_pending = 1;
+    if (!isfinite(rnorm)) {
+      sc->status = ST_DIVERGED;
+    } else if (rnorm / sc->r0 <= sc->rel_tol) {
+      sc->status = ST_CONVERGED;
+    } else {
+      sc->beta = tot / sc->rz;
+      sc->rz = tot;
+      if (k >= sc->max_iter) sc->status = ST_MAXITER;
+    }
+  }
+}
+
+// x += alpha p; p = r + beta p (solver.hpp:132,147), reference arithmetic.
+template <bool EXACT>
+__global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x, double* __restrict__ p,
+                                                          const double* __restrict__ r, long long n,
+                                                          unsigned int* done, DevScalars* sc) {
+  if (*(volatile int*)&sc->x_pending == 0) return;
+  const double alpha = sc->alpha, beta = sc->beta;
+  const bool update_p = *(volatile int*)&sc->status == ST_RUNNING;
+  const long long stride = static_cast<long long>(gridDim.x) * VT;
+  for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride) {
+    const double pi = p[i];
+    if (EXACT) {
+      x[i] = DA(x[i], DM(alpha, pi));
+      if (update_p) p[i] = DA(r[i], DM(beta, pi));
+    } else {
+      x[i] = fma(alpha, pi, x[i]);
+      if (update_p) p[i] = fma(beta, pi, r[i]);
+    }
+  }
+  if (!last_block(done)) return;
+  if (threadIdx.x == 0) {
+    sc->x_pending = 0;
+    *done = 0;
+  }
+}
+
+// ---- FUSED mode: FMA updates and fixed-order tree reductions.
+__device__ __forceinline__ double tree_partials(const double* part, int nblk, double* red) {
   double s = 0.0;
   for (int b = threadIdx.x; b < nblk; b += VT) s += __ldcg(part + b);
   return block_sum<VT>(s, red);
 }
 
-// r = b - Ap; p = r; rr = r.r; r0 = sqrt(rr) (solver.hpp:102-124).
-__global__ void __launch_bounds__(VT) cg_init_kernel(const double* __restrict__ b, const double* __restrict__ Ap,
-                                                     double* __restrict__ r, double* __restrict__ p, long long n,
-                                                     double* part, unsigned int* done, DevScalars* sc,
-                                                     double* hist, double rel_tol, int max_iter) {
+__global__ void __launch_bounds__(VT) fused_init_kernel(const double* __restrict__ b, const double* __restrict__ Ap,
+                                                        double* __restrict__ r, double* __restrict__ p, long long n,
+                                                        double* part, unsigned int* done, DevScalars* sc,
+                                                        double* hist, double rel_tol, int max_iter) {
   __shared__ double red[VT / 32];
   double acc = 0.0;
   const long long stride = static_cast<long long>(gridDim.x) * VT;
@@ -54,7 +216,7 @@ __global__ void __launch_bounds__(VT) cg_init_kernel(const double* __restrict__ 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
   if (!last_block(done)) return;
   __threadfence();
-  const double rr = reduce_partials(part, gridDim.x, red);
+  const double rr = tree_partials(part, gridDim.x, red);
   if (threadIdx.x == 0) {
     const double r0 = sqrt(rr);
     hist[0] = r0;
@@ -65,22 +227,14 @@ __global__ void __launch_bounds__(VT) cg_init_kernel(const double* __restrict__ 
     sc->max_iter = max_iter;
     sc->iterations = 0;
     sc->x_pending = 0;
-    if (!isfinite(r0))
-      sc->status = ST_DIVERGED;
-    else if (r0 == 0.0)
-      sc->status = ST_CONVERGED;
-    else if (max_iter <= 0)
-      sc->status = ST_MAXITER;
-    else
-      sc->status = ST_RUNNING;
+    sc->status = !isfinite(r0) ? ST_DIVERGED : (r0 == 0.0 ? ST_CONVERGED : (max_iter <= 0 ? ST_MAXITER : ST_RUNNING));
     *done = 0;
   }
 }
 
-// r -= alpha Ap; rr = r.r; stopping rule and beta (solver.hpp:133-147).
-__global__ void __launch_bounds__(VT) cg_update_r_kernel(const double* __restrict__ Ap, double* __restrict__ r,
-                                                         long long n, double* part, unsigned int* done,
-                                                         DevScalars* sc, double* hist) {
+__global__ void __launch_bounds__(VT) fused_update_r_kernel(const double* __restrict__ Ap, double* __restrict__ r,
+                                                            long long n, double* part, unsigned int* done,
+                                                            DevScalars* sc, double* hist) {
   __shared__ double red[VT / 32];
   if (*(volatile int*)&sc->status != ST_RUNNING) return;
   const double alpha = sc->alpha;
@@ -95,7 +249,7 @@ __global__ void __launch_bounds__(VT) cg_update_r_kernel(const double* __restric
   if (threadIdx.x == 0) part[blockIdx.x] = s;
   if (!last_block(done)) return;
   __threadfence();
-  const double rr = reduce_partials(part, gridDim.x, red);
+  const double rr = tree_partials(part, gridDim.x, red);
   if (threadIdx.x == 0) {
     const double rnorm = sqrt(rr);
     const int k = sc->iterations + 1;
@@ -108,7 +262,7 @@ __global__ void __launch_bounds__(VT) cg_update_r_kernel(const double* __restric
     } else if (rnorm / sc->r0 <= sc->rel_tol) {
       sc->status = ST_CONVERGED;
     } else {
-      sc->beta = rr / sc->rz;  // z = r: rz_next == r.r (solver.hpp:143-146)
+      sc->beta = rr / sc->rz;
       sc->rz = rr;
       if (k >= sc->max_iter) sc->status = ST_MAXITER;
     }
@@ -116,79 +270,67 @@ __global__ void __launch_bounds__(VT) cg_update_r_kernel(const double* __restric
   }
 }
 
-// x += alpha p; p = r + beta p (solver.hpp:132,147).
-__global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x, double* __restrict__ p,
-                                                          const double* __restrict__ r, long long n,
-                                                          unsigned int* done, DevScalars* sc) {
-  if (*(volatile int*)&sc->x_pending == 0) return;
-  const double alpha = sc->alpha, beta = sc->beta;
-  const bool update_p = *(volatile int*)&sc->status == ST_RUNNING;
-  const long long stride = static_cast<long long>(gridDim.x) * VT;
-  if (update_p) {
-    for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride) {
-      const double pi = p[i];
-      x[i] = fma(alpha, pi, x[i]);
-      p[i] = fma(beta, pi, r[i]);
-    }
-  } else {
-    for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride)
-      x[i] = fma(alpha, p[i], x[i]);
-  }
-  if (!last_block(done)) return;
-  if (threadIdx.x == 0) {
-    sc->x_pending = 0;
-    *done = 0;
-  }
-}
-
-__global__ void __launch_bounds__(VT) dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                                 long long n, double* part, unsigned int* done, double* out) {
-  __shared__ double red[VT / 32];
-  double acc = 0.0;
-  const long long stride = static_cast<long long>(gridDim.x) * VT;
-  for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride)
-    acc = fma(a[i], b[i], acc);
-  const double s = block_sum<VT>(acc, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
-  if (!last_block(done)) return;
-  __threadfence();
-  const double tot = reduce_partials(part, gridDim.x, red);
-  if (threadIdx.x == 0) {
-    *out = tot;
-    *done = 0;
-  }
+int chunk_grid(int64_t n) {
+  const long long nch = (n + CHUNK - 1) / CHUNK;
+  return static_cast<int>((nch + CPB - 1) / CPB);
 }
 
 }  // namespace
 
 int vec_grid(int64_t n) {
-  // Fixed function of n (never of timing): 148 SMs x 8 blocks of 256 threads,
-  // fewer for small vectors.
+  // Fixed function of n (never of timing): at most 148 SMs x 8 blocks.
   long long g = (n + VT - 1) / VT;
   if (g > 148 * 8) g = 148 * 8;
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
+int64_t reduction_partials(int64_t n) {
+  const int64_t nch = (n + CHUNK - 1) / CHUNK;
+  return nch > 148 * 8 ? nch : 148 * 8;
+}
+
 cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
                            cudaStream_t st) {
-  cg_init_kernel<<<vec_grid(n), VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials, ws.vec_done, ws.sc,
-                                             ws.history, rel_tol, max_iter);
+  if (ws.exact) {
+    blocked_reduce_kernel<OP_INIT><<<chunk_grid(n), VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials,
+                                                                 ws.vec_done, ws.sc, ws.history, nullptr, rel_tol,
+                                                                 max_iter);
+  } else {
+    fused_init_kernel<<<vec_grid(n), VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials, ws.vec_done, ws.sc,
+                                                  ws.history, rel_tol, max_iter);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st) {
+  blocked_reduce_kernel<OP_PAP><<<chunk_grid(n), VT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials,
+                                                              ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st) {
-  cg_update_r_kernel<<<vec_grid(n), VT, 0, st>>>(ws.Ap, ws.r, n, ws.vec_partials, ws.vec_done, ws.sc, ws.history);
+  if (ws.exact) {
+    blocked_reduce_kernel<OP_UPDATE_R><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
+                                                                     ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
+  } else {
+    fused_update_r_kernel<<<vec_grid(n), VT, 0, st>>>(ws.Ap, ws.r, n, ws.vec_partials, ws.vec_done, ws.sc,
+                                                      ws.history);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st) {
-  cg_update_xp_kernel<<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc);
+  if (ws.exact)
+    cg_update_xp_kernel<true><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc);
+  else
+    cg_update_xp_kernel<false><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
                        cudaStream_t st) {
-  dot_kernel<<<vec_grid(n), VT, 0, st>>>(a, b, n, ws.vec_partials, ws.vec_done, out);
+  blocked_reduce_kernel<OP_DOT><<<chunk_grid(n), VT, 0, st>>>(a, b, nullptr, nullptr, n, ws.vec_partials,
+                                                              ws.vec_done, ws.sc, ws.history, out, 0.0, 0);
   return cudaGetLastError();
 }
 

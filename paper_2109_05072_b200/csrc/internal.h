@@ -50,6 +50,7 @@ struct ApplyArgs {
   int constrained;          // ConstrainedOperator semantics (solver.hpp:60-65)
   int bc_zlo, bc_zhi;       // z-faces that are essential (slab partitions)
   double* lateral;          // ring partials [Z][column][4p]
+  double* zupper;           // exact mode: upper-layer ring partials of z-shared planes [ez][column][4p]
   double* col_dot;          // per-column partial p.Ap (nullptr: no dot)
   double* fix_partials;     // per-block partial p.Ap of the lateral fix-up
   unsigned int* fix_done;
@@ -77,6 +78,7 @@ struct Workspace {
   const Setup* s = nullptr;
   int device = 0;
   double* lateral = nullptr;
+  double* zupper = nullptr;
   double* col_dot = nullptr;
   double* fix_partials = nullptr;
   unsigned int* fix_done = nullptr;
@@ -92,6 +94,8 @@ struct Workspace {
   double* history = nullptr;
   int history_cap = 0;
   int vec_blocks = 0;
+  int exact = 1;                  // reduction mode (cg.cu): 1 = reference order, 0 = fused
+  double* dot_result = nullptr;
   DevScalars* host_sc = nullptr;  // pinned mirror
 };
 
@@ -99,12 +103,20 @@ struct Workspace {
 cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
                          double* dot_out, DevScalars* sc, cudaStream_t st);
 int fixup_grid(const Setup& s);
+// ---- apply_mma.cu (FP64 tensor-core kernel, BP3 p = 7)
+bool mma_kernel_applies(const Setup& s);
+cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st);
+void mma_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm);
+// ---- apply_exact.cu (bit-exact reference arithmetic)
+cudaError_t launch_apply_exact(const Setup& s, const ApplyArgs& a, int fix_grid, cudaStream_t st);
 void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm);
 
 // ---- cg.cu
 cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
                            cudaStream_t st);
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st);
+cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st);
+int64_t reduction_partials(int64_t n);
 cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st);
 cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
                        cudaStream_t st);

@@ -221,18 +221,30 @@ def main():
     A = hx.ConstrainedOperator(op) if bp != 1 else op
     st = torch.cuda.current_stream(dev)
 
-    # warm-up solve, then the timed fixed-iteration solve (device-resident inputs)
-    hx.cg(A, b, x, rel_tol=0.0, max_iter=W)
+    # warm-up solve, then the timed fixed-iteration solve (device-resident inputs).
+    # Headline = fast mode (FMA/DMMA operator, fused p.Ap); reference mode
+    # (bit-exact reference arithmetic) is timed beside it.
+    hx.cg(A, b, x, rel_tol=0.0, max_iter=W, mode="fast")
     x.zero_()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(st)
-        rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=K)
+        rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=K, mode="fast")
         ev1.record(st)
         torch.cuda.synchronize()
     t_dev = ev0.elapsed_time(ev1) / 1e3
     value = n * K / t_dev / 1e9
+    x.zero_()
+    hx.cg(A, b, x, rel_tol=0.0, max_iter=2, mode="reference")
+    x.zero_()
+    torch.cuda.synchronize()
+    ev0.record(st)
+    rep_ref = hx.cg(A, b, x, rel_tol=0.0, max_iter=K, mode="reference")
+    ev1.record(st)
+    torch.cuda.synchronize()
+    t_ref = ev0.elapsed_time(ev1) / 1e3
+    op.workspace().set_mode("fast")
 
     # operator kernel alone: CUDA events around R back-to-back applies on the launch stream
     u = torch.empty_like(b).uniform_(-1, 1)
@@ -264,6 +276,7 @@ def main():
     _dp = C.POINTER(C.c_double)
     repc = _lib.CGReportC()
     ws = op.workspace()
+    ws.set_mode("fast")
     L.hexbp_cg_host(setup._h, ws._h, C.cast(bh.data_ptr(), _dp), C.cast(xh.data_ptr(), _dp), n, 0.0, 2,
                     1 if bp != 1 else 0, C.byref(repc), None)
     xh.zero_()
@@ -287,7 +300,9 @@ def main():
                    "deform_amplitude": args.amplitude, "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (factors %.2f GB)" % (setup.factor_bytes / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "bp_apply_kernel (fused operator apply)",
+                     "traffic": traffic,
+                     "kernel": ("bp3_p7_mma_kernel (DMMA)" if (bp == 3 and p == 7) else "bp_apply_kernel") +
+                               " + lateral_fixup_kernel, timed together per apply",
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "algorithmic_bytes_per_launch": b_op, "apply_ms": t_apply * 1e3},
         "cg_iteration_roofline": {"algorithmic_bytes_per_iter": b_it, "achieved_GBps": b_it * K / t_dev / 1e9,
@@ -295,7 +310,10 @@ def main():
                                   "roofline_GDOFps": peak * 1e9 / (b_it / nL) / 1e9},
         "e2e": {"value": e2e, "unit": "GDOF/s", "h2d_bytes_per_step": 2 * n * 8 / K, "d2h_bytes_per_step": n * 8 / K,
                 "path": "hexbp_cg_host (C ABI, pinned host b/x; b, x0 in and x out per solve, amortised per step)"},
-        "gpu_launches": 3 * K + 2,
+        "gpu_launches": 4 * K + 3,
+        "reference_mode": {"GDOFps": n * K / t_ref / 1e9, "ms_per_step": t_ref / K * 1e3,
+                           "note": "bit-exact reference arithmetic (same iterates as the CPU reference)",
+                           "final_rel_residual": rep_ref.final_rel_residual},
         "clocks": clk.summary(),
         "kernel": kinfo,
         "setup_seconds": setup_s,
@@ -333,11 +351,11 @@ def p_sweep(bp: int, K: int, local: int):
             A = hx.ConstrainedOperator(op) if bp != 1 else op
             b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda(local)
             x = torch.zeros_like(b)
-            hx.cg(A, b, x, 0.0, 3)
+            hx.cg(A, b, x, 0.0, 3, mode="fast")
             x.zero_()
             torch.cuda.synchronize()
             t = time.perf_counter()
-            hx.cg(A, b, x, 0.0, K)
+            hx.cg(A, b, x, 0.0, K, mode="fast")
             dt = time.perf_counter() - t
             _, b_it, nL, _ = algorithmic_bytes(bp, p, dims)
             out[str(p)] = {"GDOFps": nL * K / dt / 1e9, "dofs": nL, "roofline_frac": b_it * K / dt / 1e9 / peak}

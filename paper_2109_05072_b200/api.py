@@ -213,7 +213,10 @@ class OperatorSetup:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _lib.lib().hexbp_setup_destroy(h)
+            try:
+                _lib.lib().hexbp_setup_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def l_size(self) -> int:
@@ -279,7 +282,10 @@ class Workspace:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _lib.lib().hexbp_workspace_destroy(h)
+            try:
+                _lib.lib().hexbp_workspace_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def dot(self, a, b) -> float:

@@ -37,14 +37,20 @@ namespace hxb {
 namespace {
 
 constexpr int P = 7, N = 8, Q = 9, QQ = 81;
-constexpr int NW = 4, NT = NW * 32;
+constexpr int NW = 8, NT = NW * 32;
 constexpr int GSE = (6 * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
 // shared-memory layout (doubles)
 constexpr int US_KS = 68;                 // u staging: [k][j*8+i], k-stride 68
 constexpr int US_SZ = N * US_KS;          // per buffer
 constexpr int SA_KS = 84;                 // [f][k][i + 8c] (Z->Y) and [f][b][i + 8c] (X->Y')
 constexpr int SA_F = Q * SA_KS;           // 756
-constexpr int SB_KS = 100;                // [f][i][b + 9c] (Y->X)
+// [f][i][b + 9c] (Y->X); stride = 12 (mod 16) plus an XOR-4 swizzle of the
+// pencil index on rows i >= 4 keeps both the C-tile stores (rows 2t, 2t+1)
+// and the B-fragment loads (rows t, t+4) conflict free.
+constexpr int SB_KS = 92;
+__device__ __forceinline__ int sbi(int k, int p) { return k * SB_KS + (p ^ (((k >> 2) & 1) << 2)); }
+// per-warp 3 x 8 x 8 transpose scratch, XOR-4 swizzle on rows 2,3,6,7
+__device__ __forceinline__ int scri(int a, int pl) { return a * 8 + (pl ^ (((a >> 1) & 1) << 2)); }
 constexpr int SB_F = N * SB_KS;           // 800
 constexpr int SC_KS = 68;                 // [f][c][i + 8j] (Y'->Z'), aliases SB
 constexpr int SC_F = Q * SC_KS;           // 612
@@ -192,18 +198,18 @@ __global__ void __launch_bounds__(NT, 2)
       const double r8db = quad_sum(fma(rD1, x01, rD0 * x00));
       const double r8bd = quad_sum(fma(rB1, x11, rB0 * x10));
       // SB[f][k = i][p = b + 9c]; rows b = g, cols i = 2t, 2t+1
-      double* sb = SB + g + 9 * G;
-      sb[(2 * t) * SB_KS] = bb0;
-      sb[(2 * t + 1) * SB_KS] = bb1;
-      sb[SB_F + (2 * t) * SB_KS] = db0;
-      sb[SB_F + (2 * t + 1) * SB_KS] = db1;
-      sb[2 * SB_F + (2 * t) * SB_KS] = bd0;
-      sb[2 * SB_F + (2 * t + 1) * SB_KS] = bd1;
+      const int i0 = sbi(2 * t, g + 9 * G), i1 = sbi(2 * t + 1, g + 9 * G);
+      SB[i0] = bb0;
+      SB[i1] = bb1;
+      SB[SB_F + i0] = db0;
+      SB[SB_F + i1] = db1;
+      SB[2 * SB_F + i0] = bd0;
+      SB[2 * SB_F + i1] = bd1;
       if (t == 0) {  // b = 8, k = i = g
-        double* s8 = SB + g * SB_KS + 8 + 9 * G;
-        s8[0] = r8bb;
-        s8[SB_F] = r8db;
-        s8[2 * SB_F] = r8bd;
+        const int i8 = sbi(g, 8 + 9 * G);
+        SB[i8] = r8bb;
+        SB[SB_F + i8] = r8db;
+        SB[2 * SB_F + i8] = r8bd;
       }
     }
     __syncthreads();
@@ -211,10 +217,10 @@ __global__ void __launch_bounds__(NT, 2)
     // ------------------------------------------------ phase X
     mbar_wait_parity(bar, ez & 1);
     for (int G = warp; G < 11; G += NW) {  // pencils p = 8G + (0..7) over (b,c), valid p < 81
-      const double* sb = SB + 8 * G + g;
-      const double x00 = sb[t * SB_KS], x01 = sb[(t + 4) * SB_KS];
-      const double x10 = sb[SB_F + t * SB_KS], x11 = sb[SB_F + (t + 4) * SB_KS];
-      const double x20 = sb[2 * SB_F + t * SB_KS], x21 = sb[2 * SB_F + (t + 4) * SB_KS];
+      const int k0 = sbi(t, 8 * G + g), k1 = sbi(t + 4, 8 * G + g);
+      const double x00 = SB[k0], x01 = SB[k1];
+      const double x10 = SB[SB_F + k0], x11 = SB[SB_F + k1];
+      const double x20 = SB[2 * SB_F + k0], x21 = SB[2 * SB_F + k1];
       double gr[2] = {0, 0}, gs[2] = {0, 0}, gt[2] = {0, 0};
       dmma(gr[0], gr[1], aD0, x00);
       dmma(gr[0], gr[1], aD1, x01);
@@ -252,13 +258,15 @@ __global__ void __launch_bounds__(NT, 2)
         }
       }
       // warp-local transpose of the C tiles into B-fragment order: scr[f][a][pl]
-      *reinterpret_cast<double2*>(scr + 0 * 64 + 8 * g + 2 * t) = make_double2(gr[0], gr[1]);
-      *reinterpret_cast<double2*>(scr + 1 * 64 + 8 * g + 2 * t) = make_double2(gs[0], gs[1]);
-      *reinterpret_cast<double2*>(scr + 2 * 64 + 8 * g + 2 * t) = make_double2(gt[0], gt[1]);
+      const int w0 = scri(g, 2 * t);
+      *reinterpret_cast<double2*>(scr + 0 * 64 + w0) = make_double2(gr[0], gr[1]);
+      *reinterpret_cast<double2*>(scr + 1 * 64 + w0) = make_double2(gs[0], gs[1]);
+      *reinterpret_cast<double2*>(scr + 2 * 64 + w0) = make_double2(gt[0], gt[1]);
       __syncwarp();
-      const double v00 = scr[t * 8 + g], v01 = scr[(t + 4) * 8 + g];
-      const double v10 = scr[64 + t * 8 + g], v11 = scr[64 + (t + 4) * 8 + g];
-      const double v20 = scr[128 + t * 8 + g], v21 = scr[128 + (t + 4) * 8 + g];
+      const int q0 = scri(t, g), q1 = scri(t + 4, g);
+      const double v00 = scr[q0], v01 = scr[q1];
+      const double v10 = scr[64 + q0], v11 = scr[64 + q1];
+      const double v20 = scr[128 + q0], v21 = scr[128 + q1];
       __syncwarp();
       // a = 8 values of pencils pl = 2t, 2t+1 (held by quads 2t, 2t+1)
       const double v8r0 = __shfl_sync(0xffffffffu, r8r, 8 * t), v8r1 = __shfl_sync(0xffffffffu, r8r, 8 * t + 4);

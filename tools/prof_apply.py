@@ -16,9 +16,11 @@ ap.add_argument("--p", type=int, default=7)
 ap.add_argument("--dims", default="66,66,66")
 ap.add_argument("--reps", type=int, default=6)
 ap.add_argument("--cg", type=int, default=0)
+ap.add_argument("--mode", default="fast")
 a = ap.parse_args()
 dims = tuple(int(x) for x in a.dims.split(","))
 op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(a.bp), hx.build_box_mesh(dims, a.p)))
+op.workspace().set_mode(a.mode)
 A = hx.ConstrainedOperator(op) if a.bp != 1 else op
 u = torch.empty(op.size(), dtype=torch.float64, device="cuda").uniform_(-1, 1)
 w = torch.empty_like(u)
@@ -33,5 +35,5 @@ print("kernel:", op.workspace().kernel_info())
 if a.cg:
     b = torch.from_numpy(hx.bench_rhs(a.bp, a.p, dims)).cuda()
     x = torch.zeros_like(b)
-    rep = hx.cg(A, b, x, 0.0, a.cg)
+    rep = hx.cg(A, b, x, 0.0, a.cg, mode=a.mode)
     print("cg iters", rep.iterations)

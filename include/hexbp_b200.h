@@ -148,6 +148,33 @@ int hexbp_count_flops(hexbp_setup_t s, uint64_t* mul, uint64_t* add);
  * uniform_real_distribution so the device solves the reference's system. */
 int hexbp_bench_rhs(int bp, int p, const int dims[3], uint64_t seed, int64_t offset, int64_t count, double* out);
 
+/* ---- Multi-GPU z-slab building blocks (paper_2109_05072_b200/parallel.py).
+ * The reference has no distributed path; these split hexbp_cg at its
+ * reductions so that the rank partials can be all-gathered (NCCL) and
+ * combined in rank order on every rank:
+ *   apply(p) -> halo (plane exchange + hexbp_plane_combine) ->
+ *   hexbp_cgd_reduce(PAP) -> all-gather -> hexbp_cgd_finish(PAP) ->
+ *   hexbp_cgd_reduce(UPDATE_R) -> all-gather -> hexbp_cgd_finish(UPDATE_R) ->
+ *   hexbp_cgd_update_xp.
+ * Partials sum entries [owned_offset, l_size) in deterministic_dot order. */
+enum { HEXBP_CGD_INIT = 0, HEXBP_CGD_PAP = 1, HEXBP_CGD_UPDATE_R = 2 };
+/* Device pointers of the workspace CG vectors (l_size doubles each). */
+int hexbp_workspace_vectors(hexbp_workspace_t ws, double** r, double** p, double** Ap);
+/* INIT: r = b - Ap, p = r, partial r.r; PAP: partial p.Ap; UPDATE_R: r -= alpha Ap, partial r.r.
+ * partial_dev: one device double. */
+int hexbp_cgd_reduce(hexbp_workspace_t ws, int op, const double* b_dev, int64_t owned_offset, double* partial_dev,
+                     void* stream);
+/* Rank-order sum of `world` gathered partials (device) + the scalar recurrence. */
+int hexbp_cgd_finish(hexbp_workspace_t ws, int op, const double* gathered_dev, int world, double rel_tol, int max_iter,
+                     void* stream);
+int hexbp_cgd_update_xp(hexbp_workspace_t ws, double* x_dev, void* stream);
+/* Synchronous read of the device CG state: status 0 running, 1 converged, 2 diverged, 3 max_iter. */
+int hexbp_cgd_report(hexbp_workspace_t ws, int* status, hexbp_cg_report* report, double* history, int history_cap);
+/* Halo sum of one interface node plane (nxn x nyn): dst += src, box-boundary
+ * nodes keep u when constrained. */
+int hexbp_plane_combine(double* dst_dev, const double* src_dev, const double* u_dev, int nxn, int nyn, int constrained,
+                        void* stream);
+
 /* Kernel resource report: registers/thread, static+dynamic smem bytes,
  * threads per CTA, resident CTAs per SM. */
 int hexbp_kernel_info(hexbp_setup_t s, int* regs, int* smem_bytes, int* threads, int* ctas_per_sm);

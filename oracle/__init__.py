@@ -169,6 +169,22 @@ class Oracle:
         return []
 
 
+class OracleSlab(Oracle):
+    """Element layers [z0, z1) of the (ex, ey, gez) box: the local problem of
+    one rank of the multi-GPU z-slab partition (coordinates from the global
+    box, essential nodes on the global box surface only)."""
+
+    def __init__(self, bp: int, p: int, gdims, z0: int, z1: int, amplitude: float = 0.0):
+        self.slab = (z0, z1)
+        super().__init__(bp, p, gdims, amplitude)
+
+    def _create(self, bp, p, dims, a):
+        f = self._fn("create_slab")
+        f.restype = C.c_void_p
+        f.argtypes = [C.c_int] * 7 + [C.c_double]
+        return f(bp, p, dims[0], dims[1], dims[2], self.slab[0], self.slab[1], a)
+
+
 class RefLib(Oracle):
     """The reference itself (headers compiled in place), same interface."""
 

@@ -408,9 +408,13 @@ void or_destroy(void* hv) {
 
 const char* or_last_error(void) { return g_err; }
 
-void* or_create(int bp, int p, int ex, int ey, int ez, double amplitude) {
-  if (!(bp == 1 || bp == 3 || bp == 5) || p < 1 || p > 16 || ex < 1 || ey < 1 || ez < 1 ||
-      !(amplitude >= 0.0 && amplitude <= 0.15)) {
+/* Element layers [z0, z1) of the (ex, ey, gez) box -- the multi-GPU slab
+ * partition's local problem (coordinates from the global box, essential
+ * nodes = global box surface only). or_create is the z0 = 0, z1 = gez case. */
+void* or_create_slab(int bp, int p, int ex, int ey, int gez, int z0, int z1, double amplitude) {
+  const int ez = z1 - z0;
+  if (!(bp == 1 || bp == 3 || bp == 5) || p < 1 || p > 16 || ex < 1 || ey < 1 || gez < 1 || z0 < 0 || z1 > gez ||
+      ez < 1 || !(amplitude >= 0.0 && amplitude <= 0.15)) {
     snprintf(g_err, sizeof g_err, "or_create: invalid arguments");
     return NULL;
   }
@@ -434,15 +438,16 @@ void* or_create(int bp, int p, int ex, int ey, int ez, double amplitude) {
 
   /* build_box_mesh, mesh.hpp:86-123 */
   double* axis[3];
+  const int gdim[3] = {ex, ey, gez};
   for (int d = 0; d < 3; ++d) {
-    axis[d] = malloc(sizeof(double) * h->grid[d]);
-    axis_coords(h->dims[d], p, 1.0, axis[d]);
+    axis[d] = malloc(sizeof(double) * (gdim[d] * p + 1));
+    axis_coords(gdim[d], p, 1.0, axis[d]);
   }
   h->coords = malloc(sizeof(double) * 3 * h->nL);
   for (int kz = 0; kz < h->grid[2]; ++kz)
     for (int ky = 0; ky < h->grid[1]; ++ky)
       for (int kx = 0; kx < h->grid[0]; ++kx) {
-        const double x = axis[0][kx], y = axis[1][ky], z = axis[2][kz];
+        const double x = axis[0][kx], y = axis[1][ky], z = axis[2][kz + z0 * p];
         double disp = 0.0;
         if (amplitude > 0.0)
           disp = amplitude * sin(2.0 * kPi * x / 1.0) * sin(2.0 * kPi * y / 1.0) * sin(2.0 * kPi * z / 1.0);
@@ -469,7 +474,8 @@ void* or_create(int bp, int p, int ex, int ey, int ez, double amplitude) {
   for (int kz = 0; kz < h->grid[2]; ++kz)
     for (int ky = 0; ky < h->grid[1]; ++ky)
       for (int kx = 0; kx < h->grid[0]; ++kx)
-        if (kx == 0 || kx == h->grid[0] - 1 || ky == 0 || ky == h->grid[1] - 1 || kz == 0 || kz == h->grid[2] - 1) {
+        if (kx == 0 || kx == h->grid[0] - 1 || ky == 0 || ky == h->grid[1] - 1 || kz + z0 * p == 0 ||
+            kz + z0 * p == gez * p) {
           h->essential[kx + (size_t)h->grid[0] * (ky + (size_t)h->grid[1] * kz)] = 1;
           ++nb;
         }
@@ -544,6 +550,10 @@ void* or_create(int bp, int p, int ex, int ey, int ez, double amplitude) {
     return NULL;
   }
   return h;
+}
+
+void* or_create(int bp, int p, int ex, int ey, int ez, double amplitude) {
+  return or_create_slab(bp, p, ex, ey, ez, 0, ez, amplitude);
 }
 
 int64_t or_size(void* h) { return ((Problem*)h)->nL; }

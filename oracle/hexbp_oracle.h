@@ -21,6 +21,8 @@ extern "C" {
 /* bp in {1,3,5}. Returns NULL on invalid input or degenerate geometry
  * (message via or_last_error()). */
 void* or_create(int bp, int p, int ex, int ey, int ez, double amplitude);
+/* element layers [z0, z1) of the (ex, ey, gez) box (multi-GPU slab) */
+void* or_create_slab(int bp, int p, int ex, int ey, int gez, int z0, int z1, double amplitude);
 void or_destroy(void* h);
 const char* or_last_error(void);
 

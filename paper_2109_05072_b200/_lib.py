@@ -62,6 +62,12 @@ def lib() -> C.CDLL:
         "hexbp_count_flops": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "hexbp_bench_rhs": (C.c_int, [C.c_int, C.c_int, i3, C.c_uint64, C.c_int64, C.c_int64, _dp]),
         "hexbp_kernel_info": (C.c_int, [_vp] + [C.POINTER(C.c_int)] * 4),
+        "hexbp_workspace_vectors": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+        "hexbp_cgd_reduce": (C.c_int, [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]),
+        "hexbp_cgd_finish": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_double, C.c_int, _vp]),
+        "hexbp_cgd_update_xp": (C.c_int, [_vp, _vp, _vp]),
+        "hexbp_cgd_report": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(CGReportC), _dp, C.c_int]),
+        "hexbp_plane_combine": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -473,6 +473,76 @@ int hexbp_dot(hexbp_workspace_t wh, const double* a, const double* b, int64_t n,
   return HEXBP_OK;
 }
 
+int hexbp_workspace_vectors(hexbp_workspace_t wh, double** r, double** p, double** Ap) {
+  if (!wh || !r || !p || !Ap) return invalid("null argument");
+  *r = wh->w.r;
+  *p = wh->w.p;
+  *Ap = wh->w.Ap;
+  return HEXBP_OK;
+}
+
+int hexbp_cgd_reduce(hexbp_workspace_t wh, int op, const double* b, int64_t owned, double* partial, void* stream) {
+  if (!wh || !partial || op < 0 || op > 2 || (op == 0 && !b)) return invalid("cgd_reduce: bad argument");
+  Workspace& w = wh->w;
+  if (owned < 0 || owned > w.s->nL) return invalid("cgd_reduce: owned offset outside the L-vector");
+  DeviceGuard g(w.device);
+  CK(launch_cgd_reduce(w, op, b, w.s->nL, owned, partial, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_cgd_finish(hexbp_workspace_t wh, int op, const double* gathered, int world, double rel_tol, int max_iter,
+                     void* stream) {
+  if (!wh || !gathered || world < 1 || op < 0 || op > 2) return invalid("cgd_finish: bad argument");
+  Workspace& w = wh->w;
+  DeviceGuard g(w.device);
+  if (op == 0 && max_iter + 1 > w.history_cap) {
+    CK(cudaFree(w.history));
+    w.history = nullptr;
+    w.history_cap = max_iter + 1;
+    CK(cudaMalloc(&w.history, sizeof(double) * w.history_cap));
+  }
+  CK(launch_cgd_finish(w, op, gathered, world, rel_tol, max_iter, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_cgd_update_xp(hexbp_workspace_t wh, double* x, void* stream) {
+  if (!wh || !x) return invalid("null argument");
+  DeviceGuard g(wh->w.device);
+  CK(launch_cg_update_xp(wh->w, x, wh->w.s->nL, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_cgd_report(hexbp_workspace_t wh, int* status, hexbp_cg_report* report, double* history, int cap) {
+  if (!wh) return invalid("null argument");
+  Workspace& w = wh->w;
+  DeviceGuard g(w.device);
+  CK(cudaDeviceSynchronize());
+  DevScalars hs;
+  CK(cudaMemcpy(&hs, w.sc, sizeof hs, cudaMemcpyDeviceToHost));
+  if (status) *status = hs.status;
+  if (history && cap > 0) {
+    const int m = hs.iterations + 1 < cap ? hs.iterations + 1 : cap;
+    CK(cudaMemcpy(history, w.history, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  }
+  if (report) {
+    double last = hs.r0;
+    if (hs.iterations > 0) CK(cudaMemcpy(&last, w.history + hs.iterations, sizeof(double), cudaMemcpyDeviceToHost));
+    report->iterations = hs.iterations;
+    report->converged = hs.status == ST_CONVERGED;
+    report->r0_norm = hs.r0;
+    report->final_rel_residual = hs.r0 == 0.0 ? 0.0 : last / hs.r0;
+    report->seconds = 0.0;
+  }
+  return hs.status == ST_DIVERGED ? (set_error("cg: divergence"), HEXBP_DIVERGENCE) : HEXBP_OK;
+}
+
+int hexbp_plane_combine(double* dst, const double* src, const double* u, int nxn, int nyn, int constrained,
+                        void* stream) {
+  if (!dst || !src || (constrained && !u) || nxn < 1 || nyn < 1) return invalid("plane_combine: bad argument");
+  CK(launch_plane_combine(dst, src, u, nxn, nyn, constrained, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
 int hexbp_workspace_set_mode(hexbp_workspace_t wh, int mode) {
   if (!wh || (mode != HEXBP_MODE_REFERENCE && mode != HEXBP_MODE_FAST)) return invalid("bad arithmetic mode");
   wh->w.exact = mode == HEXBP_MODE_REFERENCE;

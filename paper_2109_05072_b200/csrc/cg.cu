@@ -73,12 +73,20 @@ enum Op : int { OP_DOT = 0, OP_PAP = 1, OP_INIT = 2, OP_UPDATE_R = 3 };
 //   OP_PAP      : dot(p=a, Ap=b); alpha = rz / pAp            (solver.hpp:128-131)
 //   OP_INIT     : r = b - Ap (a=b_rhs, b=Ap, w0=r, w1=p); p = r; r.r; r0  (solver.hpp:102-124)
 //   OP_UPDATE_R : r = r - alpha Ap (a=r, b=Ap, w0=r); r.r; rnorm, stop, beta (solver.hpp:133-147)
+__device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, double rel_tol, int max_iter);
+
+// `owned` >= 0: elementwise updates run over [0, n) but only entries
+// [owned, n) enter the sum (multi-GPU slabs: the bottom interface plane is
+// owned by the rank below); the rank partial is written to *out (dist mode).
 template <int OP>
 __global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, const double* b, double* w0,
                                                             double* w1, long long n, double* part,
                                                             unsigned int* done, DevScalars* sc, double* hist,
-                                                            double* out, double rel_tol, int max_iter) {
+                                                            double* out, double rel_tol, int max_iter,
+                                                            long long owned = -1) {
   __shared__ double prod[CPB * TSTRIDE];
+  const bool dist = owned >= 0;
+  const long long lo = dist ? owned : 0;
   if (OP == OP_PAP || OP == OP_UPDATE_R) {
     if (*(volatile int*)&sc->status != ST_RUNNING) return;
   }
@@ -107,6 +115,7 @@ __global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, con
           w0[g] = r;
           pr = DM(r, r);
         }
+        if (g < lo) pr = 0.0;  // not owned by this rank
       }
       prod[c * TSTRIDE + e] = pr;
     }
@@ -127,16 +136,23 @@ __global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, con
   __threadfence();
   const double tot = serial_sum(part, nchunks);
   *done = 0;
-  if (OP == OP_DOT) {
-    *out = tot;
-  } else if (OP == OP_PAP) {
+  if (OP == OP_DOT || dist) {
+    *out = tot;  // distributed CG: the rank partial, combined by cgd_finish_kernel
+  } else {
+    scalar_logic(OP, tot, sc, hist, rel_tol, max_iter);
+  }
+}
+
+// The reference's scalar recurrence for one reduced quantity (solver.hpp:102-147).
+__device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, double rel_tol, int max_iter) {
+  if (op == OP_PAP) {
     if (!isfinite(tot) || tot <= 0.0) {
       sc->status = ST_DIVERGED;
     } else {
       sc->pAp = tot;
       sc->alpha = sc->rz / tot;
     }
-  } else if (OP == OP_INIT) {
+  } else if (op == OP_INIT) {
     const double r0 = sqrt(tot);
     hist[0] = r0;
     sc->r0 = r0;
@@ -275,7 +291,61 @@ int chunk_grid(int64_t n) {
   return static_cast<int>((nch + CPB - 1) / CPB);
 }
 
+// Multi-GPU: sum the all-gathered rank partials in rank order (identical on
+// every rank) and apply the scalar recurrence.
+__global__ void cgd_finish_kernel(int op, const double* gathered, int world, DevScalars* sc, double* hist,
+                                  double rel_tol, int max_iter) {
+  if (op != OP_INIT && *(volatile int*)&sc->status != ST_RUNNING) return;
+  double tot = 0.0;
+  for (int r = 0; r < world; ++r) tot = DA(tot, gathered[r]);
+  scalar_logic(op, tot, sc, hist, rel_tol, max_iter);
+}
+
+// Interface-plane halo sum of the z-slab partition: dst = dst + src (IEEE
+// addition commutes, so the two ranks sharing the plane obtain identical
+// sums); with ConstrainedOperator semantics the plane's box-boundary nodes
+// keep w = u (both ranks already hold u there).
+__global__ void plane_combine_kernel(double* dst, const double* src, const double* u, int nxn, int nyn,
+                                     int constrained) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nxn * nyn) return;
+  const int X = i % nxn, Y = i / nxn;
+  if (constrained && (X == 0 || X == nxn - 1 || Y == 0 || Y == nyn - 1))
+    dst[i] = u[i];
+  else
+    dst[i] = dst[i] + src[i];
+}
+
 }  // namespace
+
+cudaError_t launch_cgd_reduce(const Workspace& ws, int op, const double* b, int64_t n, int64_t owned,
+                              double* out, cudaStream_t st) {
+  const int grid = chunk_grid(n);
+  if (op == 0)
+    blocked_reduce_kernel<OP_INIT><<<grid, VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials, ws.vec_done, ws.sc,
+                                                       ws.history, out, 0.0, 0, owned);
+  else if (op == 1)
+    blocked_reduce_kernel<OP_PAP><<<grid, VT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials, ws.vec_done,
+                                                      ws.sc, ws.history, out, 0.0, 0, owned);
+  else
+    blocked_reduce_kernel<OP_UPDATE_R><<<grid, VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
+                                                           ws.vec_done, ws.sc, ws.history, out, 0.0, 0, owned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgd_finish(const Workspace& ws, int op, const double* gathered, int world, double rel_tol,
+                              int max_iter, cudaStream_t st) {
+  const int opk = op == 0 ? OP_INIT : (op == 1 ? OP_PAP : OP_UPDATE_R);
+  cgd_finish_kernel<<<1, 1, 0, st>>>(opk, gathered, world, ws.sc, ws.history, rel_tol, max_iter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plane_combine(double* dst, const double* src, const double* u, int nxn, int nyn, int constrained,
+                                 cudaStream_t st) {
+  const int n = nxn * nyn;
+  plane_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, src, u, nxn, nyn, constrained);
+  return cudaGetLastError();
+}
 
 int vec_grid(int64_t n) {
   // Fixed function of n (never of timing): at most 148 SMs x 8 blocks.

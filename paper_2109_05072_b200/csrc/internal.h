@@ -117,6 +117,12 @@ cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, doub
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st);
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st);
 int64_t reduction_partials(int64_t n);
+cudaError_t launch_cgd_reduce(const Workspace& ws, int op, const double* b, int64_t n, int64_t owned, double* out,
+                              cudaStream_t st);
+cudaError_t launch_cgd_finish(const Workspace& ws, int op, const double* gathered, int world, double rel_tol,
+                              int max_iter, cudaStream_t st);
+cudaError_t launch_plane_combine(double* dst, const double* src, const double* u, int nxn, int nyn, int constrained,
+                                 cudaStream_t st);
 cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st);
 cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
                        cudaStream_t st);

@@ -1,0 +1,86 @@
+"""The multi-GPU z-slab path with the PRODUCT kernels (CudaSlabOps: slab
+setup, apply, plane combine, cgd reduce/finish/update) on one B200: two ranks
+share cuda:0 and talk over gloo with host staging (NCCL refuses two ranks on
+one device; on a multi-GPU box bench.py --gpus N runs the same orchestration
+over NCCL). Checked against the single-domain device operator and CG."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, mode, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2109_05072_b200 as hx
+        from oracle import random_vector
+        from paper_2109_05072_b200.parallel import Comm, CudaSlabOps, DistributedOperator, SlabPartition, dist_cg
+
+        bp, p, gdims, a = case
+        torch.cuda.set_device(0)
+        mesh = hx.build_box_mesh(gdims, p, (1.0, 1.0, 1.0), a)
+        part = SlabPartition(gdims, p, world, rank)
+        ops = CudaSlabOps(hx.BPKind(bp), mesh, part, 0, mode=mode)
+        dop = DistributedOperator(part, Comm(), ops)
+        glob = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), mesh))
+        glob.workspace().set_mode(mode)
+        sl = slice(part.global_offset, part.global_offset + part.n_local)
+        u = random_vector(7, part.n_global)
+        res = {}
+        for constrained in (False, True):
+            w = torch.zeros(part.n_local, dtype=torch.float64, device="cuda")
+            dop.apply(torch.from_numpy(u[sl].copy()).cuda(), w, constrained)
+            ref = (hx.ConstrainedOperator(glob) if constrained else glob).apply(u)[sl]
+            res[f"apply{int(constrained)}"] = float(np.abs(w.cpu().numpy() - ref).max() / np.abs(ref).max())
+        b = hx.bench_rhs(bp, p, gdims)
+        x = torch.zeros(part.n_local, dtype=torch.float64, device="cuda")
+        rep = dist_cg(dop, torch.from_numpy(b[sl].copy()).cuda(), x, rel_tol=1e-8, max_iter=1000,
+                      constrained=bp != 1)
+        xg = np.zeros(part.n_global)
+        A = hx.ConstrainedOperator(glob) if bp != 1 else glob
+        ref = hx.cg(A, b, xg, rel_tol=1e-8, max_iter=1000, mode=mode)
+        res.update(iters=rep.iterations, ref_iters=ref.iterations, final=rep.final_rel_residual,
+                   ref_final=ref.final_rel_residual,
+                   xerr=float(np.abs(x.cpu().numpy() - xg[sl]).max() / np.abs(xg).max()))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,mode", [((3, 7, (4, 3, 6), 0.1), "fast"), ((3, 3, (5, 4, 6), 0.1), "reference"),
+                                       ((5, 4, (3, 3, 4), 0.1), "fast")])
+def test_two_ranks_on_one_gpu_match_single_domain(case, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, mode, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    for r in res.values():
+        assert r["apply0"] < 1e-13 and r["apply1"] < 1e-13
+        assert r["iters"] == res[0]["iters"] and r["final"] == res[0]["final"]
+        assert abs(r["iters"] - r["ref_iters"]) <= 1
+        assert r["xerr"] < 1e-7

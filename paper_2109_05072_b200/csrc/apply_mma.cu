@@ -37,7 +37,8 @@ namespace hxb {
 namespace {
 
 constexpr int P = 7, N = 8, Q = 9, QQ = 81;
-constexpr int NW = 8, NT = NW * 32;
+// 11 warps: phase X (the heaviest, 11 pencil groups) runs one group per warp.
+constexpr int NW = 11, NT = NW * 32;
 constexpr int GSE = (6 * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
 // shared-memory layout (doubles)
 constexpr int US_KS = 68;                 // u staging: [k][j*8+i], k-stride 68
@@ -335,8 +336,9 @@ __global__ void __launch_bounds__(NT, 2)
 
     // ------------------------------------------------ phase Z' + transpose restriction (part 1)
 #pragma unroll
-    for (int slot = 0; slot < N / NW; ++slot) {  // G = j; pencil i = g; contraction over c
+    for (int slot = 0; slot < (N + NW - 1) / NW; ++slot) {  // G = j; pencil i = g; contraction over c
       const int G = warp + NW * slot;
+      if (G >= N) break;  // warp-uniform
       const double* sc = SC + 8 * G + g;
       const double z00 = sc[t * SC_KS], z01 = sc[(t + 4) * SC_KS];
       const double z10 = sc[SC_F + t * SC_KS], z11 = sc[SC_F + (t + 4) * SC_KS];

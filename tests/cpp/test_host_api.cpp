@@ -1,0 +1,80 @@
+// C++ host API check on a GPU: the reference's calling pattern
+// (bench.hpp:493-518 / test_solver.cpp) against the hexbp_b200.hpp mirror.
+// Prints one line per check; exit code 0 iff all pass.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "hexbp_b200.hpp"
+
+using namespace hexbp::b200;
+
+static int failures = 0;
+#define EXPECT(cond, ...)                        \
+  do {                                           \
+    const bool ok_ = (cond);                     \
+    std::printf("[%s] ", ok_ ? "PASS" : "FAIL"); \
+    std::printf(__VA_ARGS__);                    \
+    std::printf("\n");                           \
+    if (!ok_) ++failures;                        \
+  } while (0)
+
+int main() {
+  // run_bench-style: BP3 p=3 12^3 a=0.1, constrained CG to 1e-8 (golden: 235 iterations,
+  // final 9.757368339832182e-09 -- reference mode reproduces the reference bitwise)
+  const HexMesh mesh = build_box_mesh({12, 12, 12}, 3, {1.0, 1.0, 1.0}, 0.1);
+  const OperatorHandle op(Backend::Cuda, make_setup(BPKind::BP3, mesh));
+  const ConstrainedOperator cop(op);
+  const std::vector<double> b = bench_rhs(BPKind::BP3, 3, mesh.dims);
+  std::vector<double> x(b.size(), 0.0);
+  const CGReport rep = cg(cop, b, x, 1e-8, 2000);
+  EXPECT(rep.iterations == 235 && rep.converged, "cg iterations %d (reference 235)", rep.iterations);
+  EXPECT(rep.final_rel_residual == 9.757368339832182e-09, "final rel residual %.17g", rep.final_rel_residual);
+  EXPECT(rep.residual_history.size() == 236u, "history length %zu", rep.residual_history.size());
+
+  // OperatorHandle::apply semantics: resize, linearity, symmetry, length check
+  std::mt19937_64 rng(5);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  std::vector<double> u(op.size()), v(op.size()), w, wv, wsum, s(op.size());
+  for (auto& t : u) t = dist(rng);
+  for (auto& t : v) t = dist(rng);
+  op.apply(u, w);
+  op.apply(v, wv);
+  for (int i = 0; i < op.size(); ++i) s[i] = u[i] + 2.0 * v[i];
+  op.apply(s, wsum);
+  double lin = 0.0, nrm = 0.0, uav = 0.0, vau = 0.0;
+  for (int i = 0; i < op.size(); ++i) {
+    lin = std::fmax(lin, std::fabs(wsum[i] - (w[i] + 2.0 * wv[i])));
+    nrm = std::fmax(nrm, std::fabs(wsum[i]));
+    uav += u[i] * wv[i];
+    vau += v[i] * w[i];
+  }
+  EXPECT(w.size() == u.size(), "apply resizes w");
+  EXPECT(lin <= 1e-13 * nrm, "linearity %.3e", lin / nrm);
+  EXPECT(std::fabs(uav - vau) <= 1e-12 * std::fabs(uav), "symmetry %.3e", std::fabs(uav - vau) / std::fabs(uav));
+  bool threw = false;
+  try {
+    std::vector<double> bad(3), out;
+    op.apply(bad, out);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw, "length mismatch throws std::invalid_argument (operator.hpp:268)");
+  threw = false;
+  try {
+    make_setup(BPKind::BP5, build_box_mesh({1, 1, 1}, 3, {1.0, 1.0, 1.0}, 0.1));
+  } catch (const degenerate_element_error&) {
+    threw = true;
+  }
+  EXPECT(threw, "inverted element throws degenerate_element_error (geometry.hpp:129)");
+  // fast mode: same iteration count within one, tolerance-level agreement
+  op.workspace().set_mode(Mode::Fast);
+  std::vector<double> x2(b.size(), 0.0);
+  const CGReport rf = cg(cop, b, x2, 1e-8, 2000);
+  EXPECT(std::abs(rf.iterations - 235) <= 1, "fast mode iterations %d", rf.iterations);
+  const FlopCount fc = op.count_flops();
+  EXPECT(fc.total() > 0, "count_flops %llu per element", static_cast<unsigned long long>(fc.total()));
+  std::printf("%s\n", failures ? "FAILED" : "ALL PASS");
+  return failures ? 1 : 0;
+}

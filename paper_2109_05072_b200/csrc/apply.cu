@@ -613,7 +613,8 @@ bool use_mma(const Setup& s) {
     const char* v = std::getenv("HEXBP_NO_DMMA");
     return v && *v && *v != '0';
   }();
-  return !disabled && mma_kernel_applies(s);
+  // the [qp][6] factor layout of BP3 p=7 setups is read by the DMMA kernel only
+  return (s.g_aos || !disabled) && mma_kernel_applies(s);
 }
 
 void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm) {
@@ -637,6 +638,7 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.w = w;
   a.G = s.G;
   a.gstride = s.gstride;
+  a.g_aos = s.g_aos;
   a.nx = s.dims[0];
   a.ny = s.dims[1];
   a.nz = s.dims[2];

@@ -263,9 +263,10 @@ __global__ void __launch_bounds__(XCfg<P, Q, KIND>::NT, 1)
             u = DA(u, DM(bs.D[c][k], z2[k]));
           }
           // apply_diffusion_factors (operator.hpp:129-131); G at point (a,b,c)
-          const double* g = Gs + a * QQ + b + Q * c;
-          const double g0 = g[0], g1 = g[Q * QQ], g2 = g[2 * Q * QQ], g3 = g[3 * Q * QQ], g4 = g[4 * Q * QQ],
-                       g5 = g[5 * Q * QQ];
+          const int qp = a + Q * (b + Q * c);
+          const double* g = A.g_aos ? Gs + qp * 6 : Gs + a * QQ + b + Q * c;
+          const int cs = A.g_aos ? 1 : Q * QQ;  // component stride
+          const double g0 = g[0], g1 = g[cs], g2 = g[2 * cs], g3 = g[3 * cs], g4 = g[4 * cs], g5 = g[5 * cs];
           vr[c] = DA(DA(DM(g0, r), DM(g1, s)), DM(g2, u));
           vs[c] = DA(DA(DM(g1, r), DM(g3, s)), DM(g4, u));
           vt[c] = DA(DA(DM(g2, r), DM(g4, s)), DM(g5, u));

@@ -237,9 +237,10 @@ __global__ void __launch_bounds__(NT, 2)
       for (int e = 0; e < 2; ++e) {
         const int p = 8 * G + 2 * t + e;
         if (p < QQ) {
-          const double* gp = Gs + g * QQ + p;
-          const double g0 = gp[0], g1 = gp[Q * QQ], g2 = gp[2 * Q * QQ], g3 = gp[3 * Q * QQ], g4 = gp[4 * Q * QQ],
-                       g5 = gp[5 * Q * QQ];
+          // [qp][6] block layout: three conflict-free 16-byte loads per point
+          const double2* gp = reinterpret_cast<const double2*>(Gs + (g + Q * p) * 6);
+          const double2 ga = gp[0], gb = gp[1], gc = gp[2];
+          const double g0 = ga.x, g1 = ga.y, g2 = gb.x, g3 = gb.y, g4 = gc.x, g5 = gc.y;
           const double r = gr[e], s = gs[e], u = gt[e];
           gr[e] = g0 * r + g1 * s + g2 * u;
           gs[e] = g1 * r + g3 * s + g4 * u;
@@ -249,9 +250,9 @@ __global__ void __launch_bounds__(NT, 2)
       {
         const int p = 8 * G + g;
         if (p < QQ) {
-          const double* gp = Gs + 8 * QQ + p;
-          const double g0 = gp[0], g1 = gp[Q * QQ], g2 = gp[2 * Q * QQ], g3 = gp[3 * Q * QQ], g4 = gp[4 * Q * QQ],
-                       g5 = gp[5 * Q * QQ];
+          const double2* gp = reinterpret_cast<const double2*>(Gs + (8 + Q * p) * 6);
+          const double2 ga = gp[0], gb = gp[1], gc = gp[2];
+          const double g0 = ga.x, g1 = ga.y, g2 = gb.x, g3 = gb.y, g4 = gc.x, g5 = gc.y;
           const double r = r8r, s = r8s, u = r8t;
           r8r = g0 * r + g1 * s + g2 * u;
           r8s = g1 * r + g3 * s + g4 * u;

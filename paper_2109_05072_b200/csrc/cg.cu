@@ -191,7 +191,28 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
   const double alpha = sc->alpha, beta = sc->beta;
   const bool update_p = *(volatile int*)&sc->status == ST_RUNNING;
   const long long stride = static_cast<long long>(gridDim.x) * VT;
-  for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride) {
+  long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x;
+  // 4 independent coalesced streams per thread in flight (memory-level parallelism)
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    double pv[4], xv[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pv[u] = p[i + u * stride];
+      xv[u] = x[i + u * stride];
+      rv[u] = update_p ? r[i + u * stride] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (EXACT) {
+        x[i + u * stride] = DA(xv[u], DM(alpha, pv[u]));
+        if (update_p) p[i + u * stride] = DA(rv[u], DM(beta, pv[u]));
+      } else {
+        x[i + u * stride] = fma(alpha, pv[u], xv[u]);
+        if (update_p) p[i + u * stride] = fma(beta, pv[u], rv[u]);
+      }
+    }
+  }
+  for (; i < n; i += stride) {
     const double pi = p[i];
     if (EXACT) {
       x[i] = DA(x[i], DM(alpha, pi));
@@ -256,7 +277,22 @@ __global__ void __launch_bounds__(VT) fused_update_r_kernel(const double* __rest
   const double alpha = sc->alpha;
   double acc = 0.0;
   const long long stride = static_cast<long long>(gridDim.x) * VT;
-  for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride) {
+  long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    double av[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      av[u] = Ap[i + u * stride];
+      rv[u] = r[i + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = fma(-alpha, av[u], rv[u]);
+      r[i + u * stride] = v;
+      acc = fma(v, v, acc);
+    }
+  }
+  for (; i < n; i += stride) {
     const double v = fma(-alpha, Ap[i], r[i]);
     r[i] = v;
     acc = fma(v, v, acc);

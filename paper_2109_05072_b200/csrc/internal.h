@@ -44,6 +44,7 @@ struct ApplyArgs {
   double* w;
   const double* G;          // factors, device layout (setup.cu)
   long long gstride;        // doubles per element block of G
+  int g_aos;                // element block layout: 1 = [qp][comp] (DMMA kernel), 0 = [comp][a][b+q*c]
   int nx, ny, nz;           // elements of this (slab) mesh
   int Nx, Ny, Nz;           // local node grid
   int ncols;                // nx * ny
@@ -68,6 +69,7 @@ struct Setup {
   int64_t E = 0;
   int device = 0;
   long long gstride = 0;
+  int g_aos = 0;  // see ApplyArgs::g_aos; chosen per (kind, p) at setup (setup.cu)
   double B[kMaxQ * (kMaxP + 1)] = {};
   double D[kMaxQ * (kMaxP + 1)] = {};
   double qw[kMaxQ] = {};

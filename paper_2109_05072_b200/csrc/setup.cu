@@ -30,7 +30,15 @@ namespace {
 struct GeomCfg {
   int p, n, q, comp, nx, ny, nz, z0;  // z0: global element layer offset of the slab
   long long gstride;
+  int aos;
 };
+
+// Offset of component m of quadrature point (a, b, c) inside an element block.
+__device__ __forceinline__ long long gidx(const GeomCfg& cfg, int m, int a, int b, int c) {
+  const int q = cfg.q;
+  if (cfg.aos) return static_cast<long long>(a + q * (b + q * c)) * cfg.comp + m;  // [qp][comp]
+  return static_cast<long long>(m) * q * q * q + static_cast<long long>(a) * q * q + (b + q * c);
+}
 
 // contract_dim (tensor.hpp:50-114), all threads of the CTA cooperate; each
 // output entry is produced by one thread with the reference's summation order.
@@ -142,9 +150,8 @@ __global__ void box_geometry_kernel(GeomCfg cfg, const double* __restrict__ Bg, 
     }
     const int a = qp % q, b = (qp / q) % q, cc = qp / (q * q);
     const double w = DM(DM(qw[a], qw[b]), qw[cc]);  // tensor_weight, geometry.hpp:139-143
-    const long long dst = static_cast<long long>(a) * q * q + (b + q * cc);
     if (cfg.comp == 1) {
-      Ge[dst] = DM(w, det);  // geometry.hpp:156-158
+      Ge[gidx(cfg, 0, a, b, cc)] = DM(w, det);  // geometry.hpp:156-158
     } else {
       // geometry.hpp:178-191
       const double inv[9] = {
@@ -159,7 +166,7 @@ __global__ void box_geometry_kernel(GeomCfg cfg, const double* __restrict__ Bg, 
         for (int s = r; s < 3; ++s) {
           double dot = 0.0;
           for (int k = 0; k < 3; ++k) dot = DA(dot, DM(inv[r * 3 + k], inv[s * 3 + k]));
-          Ge[static_cast<long long>(m) * q3 + dst] = DM(wd, dot);
+          Ge[gidx(cfg, m, a, b, cc)] = DM(wd, dot);
           ++m;
         }
     }
@@ -177,9 +184,9 @@ __global__ void factors_relayout_kernel(GeomCfg cfg, const double* __restrict__ 
   const long long e_ref = ex + static_cast<long long>(cfg.nx) * (ey + static_cast<long long>(cfg.ny) * ez);
   for (int l = threadIdx.x; l < q3 * comp; l += blockDim.x) {
     const int qp = l / comp, m = l % comp;
-    const int a = qp % q, bc = qp / q;
+    const int a = qp % q, b = (qp / q) % q, c = qp / (q * q);
     const long long aos = (e_ref * q3 + qp) * comp + m;
-    const long long dev = slot * cfg.gstride + static_cast<long long>(m) * q3 + static_cast<long long>(a) * q * q + bc;
+    const long long dev = slot * cfg.gstride + gidx(cfg, m, a, b, c);
     if (to_device)
       dst[dev] = src[aos];
     else
@@ -198,6 +205,7 @@ GeomCfg cfg_of(const Setup& s) {
   c.nz = s.dims[2];
   c.z0 = s.z0;
   c.gstride = s.gstride;
+  c.aos = s.g_aos;
   return c;
 }
 

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhexbp_b200.so")
+LIB_PATH = os.environ.get("HEXBP_LIB") or os.path.join(_HERE, "libhexbp_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p

@@ -21,11 +21,14 @@
 //   Z : 8 pencil groups (j)      u        -> B_z u, D_z u          (+ row 8)
 //   Y : 9 groups (c)             -> B_y B_z u, D_y B_z u, B_y D_z u (+ row 8)
 //   X : 11 groups of (b,c) lines -> gr, gs, gt; G; D_x^T, B_x^T   (+ row/col 8)
+//       in the transposed MMA form (data as the A operand), so the forward
+//       C fragment is directly the A fragment of the backward MMA (k-slot t
+//       <-> a = 2t, 2t+1): no transpose between the two x contractions
 //   Y': 9 groups (c)             -> C1 = B_y^T A1 + D_y^T A2, C2 = B_y^T A3
 //   Z': 8 groups (j)             -> out = B_z^T C1 + D_z^T C2     -> scatter
-// Shared-memory layouts are [field][k][pencil] with k-strides = 4 (mod 16)
-// doubles so that the B-fragment loads (k = lane%4 (+4), pencil = lane/4)
-// are bank-conflict free.
+// Shared-memory layouts are [field][k][pencil] with strides / XOR swizzles
+// chosen so that the B-fragment loads (k = lane%4 (+4), pencil = lane/4) and
+// the 16-byte C-fragment stores are bank-conflict free.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,24 +46,28 @@ constexpr int GSE = (6 * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setu
 // shared-memory layout (doubles)
 constexpr int US_KS = 68;                 // u staging: [k][j*8+i], k-stride 68
 constexpr int US_SZ = N * US_KS;          // per buffer
-constexpr int SA_KS = 84;                 // [f][k][i + 8c] (Z->Y) and [f][b][i + 8c] (X->Y')
-constexpr int SA_F = Q * SA_KS;           // 756
+// SA: [f][row][8c + i] with row stride 72 (= 8 mod 16 doubles) and the i-bit-2
+// swizzle swa(row); used for Z->Y (row = j, c = a3) and X'->Y' (row = b = a2,
+// c = a3). Both the 16-byte C-fragment stores (rows fixed per warp, pencil
+// pairs i = 2t, 2t+1) and the 8-byte B-fragment loads (rows t, t+4, i = g) are
+// bank-conflict free.
+constexpr int SA_KS = 72;
+constexpr int SA_F = Q * SA_KS;           // 648
+__device__ __forceinline__ int swa(int row) { return (row & 2) << 1; }
 // [f][i][b + 9c] (Y->X); stride = 12 (mod 16) plus an XOR-4 swizzle of the
 // pencil index on rows i >= 4 keeps both the C-tile stores (rows 2t, 2t+1)
 // and the B-fragment loads (rows t, t+4) conflict free.
 constexpr int SB_KS = 92;
 __device__ __forceinline__ int sbi(int k, int p) { return k * SB_KS + (p ^ (((k >> 2) & 1) << 2)); }
-// per-warp 3 x 8 x 8 transpose scratch, XOR-4 swizzle on rows 2,3,6,7
-__device__ __forceinline__ int scri(int a, int pl) { return a * 8 + (pl ^ (((a >> 1) & 1) << 2)); }
-constexpr int SB_F = N * SB_KS;           // 800
+constexpr int SB_F = N * SB_KS;           // 736
 constexpr int SC_KS = 68;                 // [f][c][i + 8j] (Y'->Z'), aliases SB
 constexpr int SC_F = Q * SC_KS;           // 612
 constexpr int OFF_SA = 0;
 constexpr int OFF_SB = OFF_SA + 3 * SA_F;
 constexpr int OFF_G = OFF_SB + 3 * SB_F;  // 16-byte aligned (even)
 constexpr int OFF_U = OFF_G + GSE;
-constexpr int OFF_SCR = OFF_U + 2 * US_SZ;   // per-warp 3 x 8 x 8 transpose scratch
-constexpr int OFF_BAR = OFF_SCR + NW * 192;
+constexpr int OFF_BAS = OFF_U + 2 * US_SZ;  // B, D (q x n each), resident
+constexpr int OFF_BAR = OFF_BAS + 2 * Q * N;
 constexpr int SMEM_BYTES = (OFF_BAR + 1) * 8;
 static_assert(OFF_G % 2 == 0, "TMA destination must be 16-byte aligned");
 static_assert(3 * SB_F >= 2 * SC_F, "SC aliases SB");
@@ -74,6 +81,12 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double lds_volatile(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+  return v;
 }
 
 // sum over the 4 lanes of a quad (lanes sharing lane/4)
@@ -97,7 +110,6 @@ __global__ void __launch_bounds__(NT, 2)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  double* scr = smem + OFF_SCR + warp * 192;
   const uint64_t pol = policy_evict_first();
   const bool do_dot = A.col_dot != nullptr;
   const int col = blockIdx.x;
@@ -105,13 +117,28 @@ __global__ void __launch_bounds__(NT, 2)
   const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
 
   // basis fragments, resident for the whole kernel
-  const double aB0 = bs.B[g][t], aB1 = bs.B[g][t + 4];            // forward rows 0..7 (A = M[m][k])
-  const double aD0 = bs.D[g][t], aD1 = bs.D[g][t + 4];
-  const double rB0 = bs.B[8][t], rB1 = bs.B[8][t + 4];            // forward row 8
-  const double rD0 = bs.D[8][t], rD1 = bs.D[8][t + 4];
-  const double tB0 = bs.B[t][g], tB1 = bs.B[t + 4][g];            // backward (A = M^T[i][a])
-  const double tD0 = bs.D[t][g], tD1 = bs.D[t + 4][g];
-  const double cB8 = bs.B[8][g], cD8 = bs.D[8][g];                // backward column a = 8
+  // Basis: B and D stay in shared memory for the whole kernel. The 8 x 8
+  // MMA fragments are read once into registers with volatile loads (read from
+  // the parameter bank with a lane-dependent index, ptxas would re-issue
+  // serialised LDCs inside the loop); the row-8 values (4-8 distinct
+  // addresses per warp: broadcast loads) are read from shared memory at use.
+  double* sB = smem + OFF_BAS;
+  double* sD = sB + Q * N;
+  if (tid < Q * N) {
+    sB[tid] = (&bs.B[0][0])[tid];
+    sD[tid] = (&bs.D[0][0])[tid];
+  }
+  __syncthreads();
+  auto bas = [&](const double* m, int a, int i) { return lds_volatile(m + a * N + i); };
+  const double aB0 = bas(sB, g, t), aB1 = bas(sB, g, t + 4);            // forward rows 0..7 (A = M[m][k])
+  const double aD0 = bas(sD, g, t), aD1 = bas(sD, g, t + 4);
+  const double tB0 = bas(sB, t, g), tB1 = bas(sB, t + 4, g);            // backward (A = M^T[i][a])
+  const double tD0 = bas(sD, t, g), tD1 = bas(sD, t + 4, g);
+  // phase X' (transposed form, k-slot t <-> a = 2t (+1)): B[k][n = i] = M[a][i]
+  const double eB0 = bas(sB, 2 * t, g), eB1 = bas(sB, 2 * t + 1, g);
+  const double eD0 = bas(sD, 2 * t, g), eD1 = bas(sD, 2 * t + 1, g);
+  const double* rB = sB + 8 * N;  // row a = 8
+  const double* rD = sD + 8 * N;
 
   const double* Gcol = A.G + static_cast<long long>(col) * A.nz * GSE;
   constexpr uint32_t gbytes = GSE * 8;
@@ -171,21 +198,23 @@ __global__ void __launch_bounds__(NT, 2)
       dmma(cb0, cb1, aB1, b[1]);
       dmma(cd0, cd1, aD0, b[0]);
       dmma(cd0, cd1, aD1, b[1]);
-      const double r8b = quad_sum(fma(rB1, b[1], rB0 * b[0]));
-      const double r8d = quad_sum(fma(rD1, b[1], rD0 * b[0]));
+      const double r8b = quad_sum(fma(rB[t + 4], b[1], rB[t] * b[0]));
+      const double r8d = quad_sum(fma(rD[t + 4], b[1], rD[t] * b[0]));
+      // SA[f][j = G][8 a3 + i]: rows a3 = g, cols i = 2t, 2t+1; row a3 = 8 at i = g
       double* sa = SA + G * SA_KS;
-      *reinterpret_cast<double2*>(sa + 8 * g + 2 * t) = make_double2(cb0, cb1);
-      *reinterpret_cast<double2*>(sa + SA_F + 8 * g + 2 * t) = make_double2(cd0, cd1);
+      const int h = swa(G);
+      *reinterpret_cast<double2*>(sa + 8 * g + (2 * t ^ h)) = make_double2(cb0, cb1);
+      *reinterpret_cast<double2*>(sa + SA_F + 8 * g + (2 * t ^ h)) = make_double2(cd0, cd1);
       if (t == 0) {
-        sa[64 + g] = r8b;
-        sa[SA_F + 64 + g] = r8d;
+        sa[64 + (g ^ h)] = r8b;
+        sa[SA_F + 64 + (g ^ h)] = r8d;
       }
     }
     __syncthreads();
 
     // ------------------------------------------------ phase Y
     for (int G = warp; G < Q; G += NW) {  // G = c; pencil i = g
-      const double* sa = SA + 8 * G + g;
+      const double* sa = SA + 8 * G + (g ^ swa(t));  // rows j = t, t+4 share the swizzle
       const double x00 = sa[t * SA_KS], x01 = sa[(t + 4) * SA_KS];
       const double x10 = sa[SA_F + t * SA_KS], x11 = sa[SA_F + (t + 4) * SA_KS];
       double bb0 = 0, bb1 = 0, db0 = 0, db1 = 0, bd0 = 0, bd1 = 0;
@@ -195,9 +224,9 @@ __global__ void __launch_bounds__(NT, 2)
       dmma(db0, db1, aD1, x01);
       dmma(bd0, bd1, aB0, x10);
       dmma(bd0, bd1, aB1, x11);
-      const double r8bb = quad_sum(fma(rB1, x01, rB0 * x00));
-      const double r8db = quad_sum(fma(rD1, x01, rD0 * x00));
-      const double r8bd = quad_sum(fma(rB1, x11, rB0 * x10));
+      const double r8bb = quad_sum(fma(rB[t + 4], x01, rB[t] * x00));
+      const double r8db = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));
+      const double r8bd = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
       // SB[f][k = i][p = b + 9c]; rows b = g, cols i = 2t, 2t+1
       const int i0 = sbi(2 * t, g + 9 * G), i1 = sbi(2 * t + 1, g + 9 * G);
       SB[i0] = bb0;
@@ -216,88 +245,67 @@ __global__ void __launch_bounds__(NT, 2)
     __syncthreads();
 
     // ------------------------------------------------ phase X
+    // Transposed MMA form: C^T[pencil][a] = sum_i X^T[pencil][i] M^T[i][a], so
+    // lane (g, t) ends with pencil g at points a = 2t, 2t+1 -- exactly the
+    // A-fragment (row g, k-slot t <-> a = 2t / 2t+1) of the backward MMA. No
+    // transpose between the forward and backward x contractions.
     mbar_wait_parity(bar, ez & 1);
-    for (int G = warp; G < 11; G += NW) {  // pencils p = 8G + (0..7) over (b,c), valid p < 81
+    for (int G = warp; G < 11; G += NW) {  // pencils p = 8G + g over (b, c), valid p < 81
       const int k0 = sbi(t, 8 * G + g), k1 = sbi(t + 4, 8 * G + g);
       const double x00 = SB[k0], x01 = SB[k1];
       const double x10 = SB[SB_F + k0], x11 = SB[SB_F + k1];
       const double x20 = SB[2 * SB_F + k0], x21 = SB[2 * SB_F + k1];
       double gr[2] = {0, 0}, gs[2] = {0, 0}, gt[2] = {0, 0};
-      dmma(gr[0], gr[1], aD0, x00);
-      dmma(gr[0], gr[1], aD1, x01);
-      dmma(gs[0], gs[1], aB0, x10);
-      dmma(gs[0], gs[1], aB1, x11);
-      dmma(gt[0], gt[1], aB0, x20);
-      dmma(gt[0], gt[1], aB1, x21);
-      double r8r = quad_sum(fma(rD1, x01, rD0 * x00));
-      double r8s = quad_sum(fma(rB1, x11, rB0 * x10));
-      double r8t = quad_sum(fma(rB1, x21, rB0 * x20));
-      // pointwise factors (operator.hpp:129-131) at (a = g, p = 8G+2t+e) and (a = 8, p = 8G+g)
+      dmma(gr[0], gr[1], x00, aD0);
+      dmma(gr[0], gr[1], x01, aD1);
+      dmma(gs[0], gs[1], x10, aB0);
+      dmma(gs[0], gs[1], x11, aB1);
+      dmma(gt[0], gt[1], x20, aB0);
+      dmma(gt[0], gt[1], x21, aB1);
+      double r8r = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));  // a = 8 of pencil g (all 4 lanes)
+      double r8s = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
+      double r8t = quad_sum(fma(rB[t + 4], x21, rB[t] * x20));
+      const int p = 8 * G + g;
+      if (p < QQ) {
+        // pointwise factors (operator.hpp:129-131); [qp][6] layout, qp = a + 9p:
+        // points a = 2t, 2t+1 are 12 contiguous doubles (conflict-free 16-byte loads)
+        const double2* gp = reinterpret_cast<const double2*>(Gs + (2 * t + Q * p) * 6);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int p = 8 * G + 2 * t + e;
-        if (p < QQ) {
-          // [qp][6] block layout: three conflict-free 16-byte loads per point
-          const double2* gp = reinterpret_cast<const double2*>(Gs + (g + Q * p) * 6);
-          const double2 ga = gp[0], gb = gp[1], gc = gp[2];
-          const double g0 = ga.x, g1 = ga.y, g2 = gb.x, g3 = gb.y, g4 = gc.x, g5 = gc.y;
-          const double r = gr[e], s = gs[e], u = gt[e];
-          gr[e] = g0 * r + g1 * s + g2 * u;
-          gs[e] = g1 * r + g3 * s + g4 * u;
-          gt[e] = g2 * r + g4 * s + g5 * u;
+        for (int e = 0; e < 2; ++e) {
+          const double2 ga = gp[3 * e], gb = gp[3 * e + 1], gc = gp[3 * e + 2];
+          const double r = gr[e], s_ = gs[e], u = gt[e];
+          gr[e] = ga.x * r + ga.y * s_ + gb.x * u;
+          gs[e] = ga.y * r + gb.y * s_ + gc.x * u;
+          gt[e] = gb.x * r + gc.x * s_ + gc.y * u;
         }
+        const double2* g8 = reinterpret_cast<const double2*>(Gs + (8 + Q * p) * 6);
+        const double2 ga = g8[0], gb = g8[1], gc = g8[2];
+        const double r = r8r, s_ = r8s, u = r8t;
+        r8r = ga.x * r + ga.y * s_ + gb.x * u;
+        r8s = ga.y * r + gb.y * s_ + gc.x * u;
+        r8t = gb.x * r + gc.x * s_ + gc.y * u;
       }
-      {
-        const int p = 8 * G + g;
-        if (p < QQ) {
-          const double2* gp = reinterpret_cast<const double2*>(Gs + (8 + Q * p) * 6);
-          const double2 ga = gp[0], gb = gp[1], gc = gp[2];
-          const double g0 = ga.x, g1 = ga.y, g2 = gb.x, g3 = gb.y, g4 = gc.x, g5 = gc.y;
-          const double r = r8r, s = r8s, u = r8t;
-          r8r = g0 * r + g1 * s + g2 * u;
-          r8s = g1 * r + g3 * s + g4 * u;
-          r8t = g2 * r + g4 * s + g5 * u;
-        }
-      }
-      // warp-local transpose of the C tiles into B-fragment order: scr[f][a][pl]
-      const int w0 = scri(g, 2 * t);
-      *reinterpret_cast<double2*>(scr + 0 * 64 + w0) = make_double2(gr[0], gr[1]);
-      *reinterpret_cast<double2*>(scr + 1 * 64 + w0) = make_double2(gs[0], gs[1]);
-      *reinterpret_cast<double2*>(scr + 2 * 64 + w0) = make_double2(gt[0], gt[1]);
-      __syncwarp();
-      const int q0 = scri(t, g), q1 = scri(t + 4, g);
-      const double v00 = scr[q0], v01 = scr[q1];
-      const double v10 = scr[64 + q0], v11 = scr[64 + q1];
-      const double v20 = scr[128 + q0], v21 = scr[128 + q1];
-      __syncwarp();
-      // a = 8 values of pencils pl = 2t, 2t+1 (held by quads 2t, 2t+1)
-      const double v8r0 = __shfl_sync(0xffffffffu, r8r, 8 * t), v8r1 = __shfl_sync(0xffffffffu, r8r, 8 * t + 4);
-      const double v8s0 = __shfl_sync(0xffffffffu, r8s, 8 * t), v8s1 = __shfl_sync(0xffffffffu, r8s, 8 * t + 4);
-      const double v8t0 = __shfl_sync(0xffffffffu, r8t, 8 * t), v8t1 = __shfl_sync(0xffffffffu, r8t, 8 * t + 4);
-      double a1[2], a2[2], a3[2];
-      a1[0] = cD8 * v8r0;
-      a1[1] = cD8 * v8r1;
-      a2[0] = cB8 * v8s0;
-      a2[1] = cB8 * v8s1;
-      a3[0] = cB8 * v8t0;
-      a3[1] = cB8 * v8t1;
-      dmma(a1[0], a1[1], tD0, v00);
-      dmma(a1[0], a1[1], tD1, v01);
-      dmma(a2[0], a2[1], tB0, v10);
-      dmma(a2[0], a2[1], tB1, v11);
-      dmma(a3[0], a3[1], tB0, v20);
-      dmma(a3[0], a3[1], tB1, v21);
-      // rows i = g, cols p = 8G+2t+e -> SA'[f][b][i + 8c]
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int p = 8 * G + 2 * t + e;
-        if (p < QQ) {
-          const int c = p / 9, bq = p - 9 * c;
-          double* d = SA + bq * SA_KS + g + 8 * c;
-          d[0] = a1[e];
-          d[SA_F] = a2[e];
-          d[2 * SA_F] = a3[e];
-        }
+      // backward: W[p][i] = sum_a A[p][a] M[a][i]; a = 8 term first
+      double w1[2], w2[2], w3[2];
+      w1[0] = rD[2 * t] * r8r;
+      w1[1] = rD[2 * t + 1] * r8r;
+      w2[0] = rB[2 * t] * r8s;
+      w2[1] = rB[2 * t + 1] * r8s;
+      w3[0] = rB[2 * t] * r8t;
+      w3[1] = rB[2 * t + 1] * r8t;
+      dmma(w1[0], w1[1], gr[0], eD0);
+      dmma(w1[0], w1[1], gr[1], eD1);
+      dmma(w2[0], w2[1], gs[0], eB0);
+      dmma(w2[0], w2[1], gs[1], eB1);
+      dmma(w3[0], w3[1], gt[0], eB0);
+      dmma(w3[0], w3[1], gt[1], eB1);
+      // pencil p = b + 9c, outputs i = 2t, 2t+1 -> SA[f][b][8c + i] (16-byte stores)
+      if (p < QQ) {
+        const int c = p / 9, bq = p - 9 * c;
+        double* d = SA + bq * SA_KS + 8 * c + (2 * t ^ swa(bq));
+        *reinterpret_cast<double2*>(d) = make_double2(w1[0], w1[1]);
+        *reinterpret_cast<double2*>(d + SA_F) = make_double2(w2[0], w2[1]);
+        *reinterpret_cast<double2*>(d + 2 * SA_F) = make_double2(w3[0], w3[1]);
       }
     }
     __syncthreads();
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(NT, 2)
 
     // ------------------------------------------------ phase Y'
     for (int G = warp; G < Q; G += NW) {  // G = c; pencil i = g; contraction over b
-      const double* sa = SA + 8 * G + g;
+      const double* sa = SA + 8 * G + (g ^ swa(t));
       const double y00 = sa[t * SA_KS], y01 = sa[(t + 4) * SA_KS];
       const double y10 = sa[SA_F + t * SA_KS], y11 = sa[SA_F + (t + 4) * SA_KS];
       const double y20 = sa[2 * SA_F + t * SA_KS], y21 = sa[2 * SA_F + (t + 4) * SA_KS];
@@ -318,10 +326,10 @@ __global__ void __launch_bounds__(NT, 2)
       const double2 e2 = *reinterpret_cast<const double2*>(s8 + SA_F);
       const double2 e3 = *reinterpret_cast<const double2*>(s8 + 2 * SA_F);
       double c1[2], c2[2];
-      c1[0] = fma(cD8, e2.x, cB8 * e1.x);
-      c1[1] = fma(cD8, e2.y, cB8 * e1.y);
-      c2[0] = cB8 * e3.x;
-      c2[1] = cB8 * e3.y;
+      c1[0] = fma(rD[g], e2.x, rB[g] * e1.x);
+      c1[1] = fma(rD[g], e2.y, rB[g] * e1.y);
+      c2[0] = rB[g] * e3.x;
+      c2[1] = rB[g] * e3.y;
       dmma(c1[0], c1[1], tB0, y00);
       dmma(c1[0], c1[1], tB1, y01);
       dmma(c1[0], c1[1], tD0, y10);
@@ -347,8 +355,8 @@ __global__ void __launch_bounds__(NT, 2)
       const double2 e1 = *reinterpret_cast<const double2*>(s8);
       const double2 e2 = *reinterpret_cast<const double2*>(s8 + SC_F);
       double o[2];
-      o[0] = fma(cD8, e2.x, cB8 * e1.x);
-      o[1] = fma(cD8, e2.y, cB8 * e1.y);
+      o[0] = fma(rD[g], e2.x, rB[g] * e1.x);
+      o[1] = fma(rD[g], e2.y, rB[g] * e1.y);
       dmma(o[0], o[1], tB0, z00);
       dmma(o[0], o[1], tB1, z01);
       dmma(o[0], o[1], tD0, z10);

@@ -13,18 +13,19 @@
 // elements and marches it along z. The structured-mesh gather is index
 // arithmetic (mesh.hpp:81); no connectivity table is read.
 //
-// Deterministic, atomic-free transpose restriction (K4), two launches:
-//  1. bp_apply_kernel: z-shared node planes are summed in registers (carry of
-//     the previous element's top plane, element order). Nodes strictly inside
-//     the column's (p+1)x(p+1) footprint belong to it alone: final values are
+// Deterministic transpose restriction (K4), one launch:
+//  1. z-shared node planes are summed in registers (carry of the previous
+//     element's top plane, element order). Nodes strictly inside the
+//     column's (p+1)x(p+1) footprint belong to it alone: final values are
 //     written to w once. Each of the 4p "ring" nodes of the footprint is shared
 //     with 1-3 neighbouring columns: the column writes its partial to the
 //     lateral buffer lat[Z][column][ring position].
-//  2. lateral_fixup_kernel: every ring node sums its 1-4 partials in ascending
-//     column order and writes w (and finishes p.Ap / alpha in CG mode).
+//  2. the ring nodes sum their 1-4 column partials in ascending column order
+//     (ring.cuh): lateral_fixup_kernel for plain applies; inside the CG
+//     r-update for CG (cg.cu). p.Ap and alpha are complete after part 1.
 // Every node's partials are therefore added in one fixed order: results are
 // bitwise identical run to run (restriction.hpp:18-21) with no inter-CTA
-// waiting inside the operator kernel.
+// waiting.
 //
 // Element pipeline (q x q threads per column, z-pencil -> y -> x pencils):
 //   Z : thread (i,j) holds u(i,j,:) in registers; B_z u, D_z u        -> smem A
@@ -43,6 +44,7 @@
 
 #include "device_util.cuh"
 #include "internal.h"
+#include "ring.cuh"
 
 namespace hxb {
 
@@ -142,8 +144,12 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
   const int X = ex * P + zi, Y = ey * P + zj;
   const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
   const bool ring = zi == 0 || zi == P || zj == 0 || zj == P;
-  double* lat = A.lateral + static_cast<long long>(col) * (4 * P) + ring_index(P, zi, zj);
-  const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
+  const bool owner = ring_owner(P, zi, zj, ex, ey, A.nx, A.ny);
+  const LatLayout L(P, A.nx, A.ny);
+  bool lat_is_y = false;
+  const long long lat0 = ring ? lat_store_index(L, P, A.nx, ex, ey, zi, zj, 0, lat_is_y) : 0;
+  double* lat = (lat_is_y ? A.lateral : A.lat_x) + lat0;
+  const long long lat_stride = lat_is_y ? L.y_zstride : L.x_zstride;
   double carry = 0.0, dot = 0.0;
 
   // Staging: the element's factor block G_e is copied global -> shared by the
@@ -421,6 +427,15 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
           const int Z = ez * P + k;
           if (ring) {
             lat[Z * lat_stride] = out[k];
+            if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
+              const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+              const double uv = __ldg(A.u + node);
+              if (bcxy || (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)))) {
+                if (owner) dot = fma(uv, uv, dot);  // w = u, counted once
+              } else {
+                dot = fma(uv, out[k], dot);
+              }
+            }
           } else {
             const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
             double v = out[k];
@@ -434,84 +449,36 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
     }
     __syncthreads();  // smem A is rewritten by the next element's phase Z
   }
-  if (do_dot) {
-    const double s = block_sum<NT>(dot, s_red);
-    if (t == 0) A.col_dot[col] = s;
-  }
+  const double cdot = do_dot ? block_sum<NT>(dot, s_red) : 0.0;
+  ring_dot_finish<NT>(A, col, cdot, s_red);
 }
 
-// Transpose restriction, part 2: sum the 1-4 column partials of every ring
-// node in ascending column order. In CG mode also finish p.Ap (column
-// partials of part 1 + this kernel's block partials, both in index order)
-// and alpha = rz / pAp (solver.hpp:127-131).
+// Transpose restriction, part 2, for plain applies: every ring node sums its
+// 1-4 column partials in ascending column order (ring.cuh). (CG fuses this
+// into its r-update, cg.cu; p.Ap is complete after part 1.)
 constexpr int FT = 256;
 
 __global__ void __launch_bounds__(FT) lateral_fixup_kernel(const __grid_constant__ ApplyArgs A, int P) {
-  __shared__ double red[FT / 32];
-  if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
-  const bool do_dot = A.col_dot != nullptr;
-  const long long rowpart = static_cast<long long>(A.ny + 1) * A.Nx;          // nodes on rows Y % P == 0
-  const long long colpart = static_cast<long long>(A.nx + 1) * (A.ny * (P - 1));  // X % P == 0, Y % P != 0
-  const long long per_plane = rowpart + colpart;
-  const long long total = per_plane * A.Nz;
-  const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
-  double dot = 0.0;
-  for (long long l = blockIdx.x * static_cast<long long>(FT) + threadIdx.x; l < total;
-       l += static_cast<long long>(gridDim.x) * FT) {
-    const int Z = static_cast<int>(l / per_plane);
-    const long long r = l - static_cast<long long>(Z) * per_plane;
-    int X, Y;
-    if (r < rowpart) {
-      Y = static_cast<int>(r / A.Nx) * P;
-      X = static_cast<int>(r % A.Nx);
-    } else {
-      const long long r2 = r - rowpart;
-      const int yy = static_cast<int>(r2 / (A.nx + 1));
-      X = static_cast<int>(r2 % (A.nx + 1)) * P;
-      Y = (yy / (P - 1)) * P + 1 + yy % (P - 1);
-    }
-    // contributing columns in ascending index order
-    const int ex_hi = X / P < A.nx ? X / P : A.nx - 1;
-    const int ex_lo = (X % P == 0 && X > 0) ? X / P - 1 : ex_hi;
-    const int ey_hi = Y / P < A.ny ? Y / P : A.ny - 1;
-    const int ey_lo = (Y % P == 0 && Y > 0) ? Y / P - 1 : ey_hi;
-    const double* latZ = A.lateral + Z * lat_stride;
-    double s = 0.0;
-    for (int cy = ey_lo; cy <= ey_hi; ++cy)
-      for (int cx = ex_lo; cx <= ex_hi; ++cx)
-        s += latZ[static_cast<long long>(cy * A.nx + cx) * (4 * P) + ring_index(P, X - cx * P, Y - cy * P)];
-    const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-    if (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1 || (Z == 0 && A.bc_zlo) ||
-                          (Z == A.Nz - 1 && A.bc_zhi)))
-      s = A.u[node];
-    A.w[node] = s;
-    if (do_dot) dot = fma(A.u[node], s, dot);
-  }
-  if (!do_dot) return;
-  const double bsum = block_sum<FT>(dot, red);
-  __shared__ int s_last;
-  if (threadIdx.x == 0) {
-    A.fix_partials[blockIdx.x] = bsum;
-    __threadfence();
-    s_last = atomicAdd(A.fix_done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  double s = 0.0;
-  for (int c = threadIdx.x; c < A.ncols; c += FT) s += __ldcg(A.col_dot + c);
-  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += FT) s += __ldcg(A.fix_partials + b);
-  const double pAp = block_sum<FT>(s, red);
-  if (threadIdx.x == 0) {
-    *A.fix_done = 0;
-    if (A.dot_out) *A.dot_out = pAp;
-    if (A.sc) {
-      if (!isfinite(pAp) || pAp <= 0.0) {
-        A.sc->status = ST_DIVERGED;
-      } else {
-        A.sc->pAp = pAp;
-        A.sc->alpha = A.sc->rz / pAp;
-      }
+  // one warp per node row (Y, Z): ring rows (Y % P == 0) finish every node,
+  // other rows their x-face nodes X = fx*P
+  const LatLayout L(P, A.nx, A.ny);
+  const int lane = threadIdx.x & 31;
+  const long long rows = static_cast<long long>(A.Ny) * A.Nz;
+  for (long long row = blockIdx.x * (FT / 32) + (threadIdx.x >> 5); row < rows;
+       row += static_cast<long long>(gridDim.x) * (FT / 32)) {
+    const int Z = static_cast<int>(row / A.Ny), Y = static_cast<int>(row - static_cast<long long>(Z) * A.Ny);
+    const bool yring = Y % P == 0;
+    const int count = yring ? A.Nx : A.nx + 1;
+    const bool bcrow = A.constrained && (Y == 0 || Y == A.Ny - 1 || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+    for (int q = lane; q < count; q += 32) {
+      const int X = yring ? q : q * P;
+      const long long node = X + static_cast<long long>(A.Nx) * row;
+      double s;
+      if (A.constrained && (bcrow || X == 0 || X == A.Nx - 1))
+        s = A.u[node];
+      else
+        s = ring_node_sum(A.lateral, A.lat_x, L, P, A.nx, A.ny, X, Y, Z);
+      A.w[node] = s;
     }
   }
 }
@@ -632,7 +599,7 @@ void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* 
 }
 
 cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
-                         double* dot_out, DevScalars* sc, cudaStream_t st) {
+                         double* dot_out, DevScalars* sc, cudaStream_t st, bool finish_ring) {
   ApplyArgs a{};
   a.u = u;
   a.w = w;
@@ -650,6 +617,7 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.bc_zlo = s.bc_zlo;
   a.bc_zhi = s.bc_zhi;
   a.lateral = ws.lateral;
+  a.lat_x = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
   a.zupper = ws.zupper;
   a.col_dot = (dot_out || sc) ? ws.col_dot : nullptr;
   a.fix_partials = ws.fix_partials;
@@ -670,7 +638,7 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
       case KIND_COLLOC: e = launch_k<KIND_COLLOC>(s, a, st); break;
     }
   }
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || !finish_ring) return e;  // CG: the r-update sums the ring (cg.cu)
   lateral_fixup_kernel<<<ws.fixup_grid, FT, 0, st>>>(a, s.p);
   return cudaGetLastError();
 }

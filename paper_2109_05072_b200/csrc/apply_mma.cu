@@ -35,6 +35,7 @@
 
 #include "device_util.cuh"
 #include "internal.h"
+#include "ring.cuh"
 
 namespace hxb {
 namespace {
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(NT, 2)
   const bool do_dot = A.col_dot != nullptr;
   const int col = blockIdx.x;
   const int ex = col % A.nx, ey = col / A.nx;
-  const long long lat_stride = static_cast<long long>(A.ncols) * (4 * P);
+  const LatLayout Lat(P, A.nx, A.ny);
 
   // basis fragments, resident for the whole kernel
   // Basis: B and D stay in shared memory for the whole kernel. The 8 x 8
@@ -375,23 +376,39 @@ __global__ void __launch_bounds__(NT, 2)
       }
       const int Z = ez * P + g, Y = ey * P + G;
       const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+      // u at these nodes: still staged in shared memory (z-plane k = g of this element)
+      const double2 u2 = *reinterpret_cast<const double2*>(us + g * US_KS + G * 8 + 2 * t);
+      // ring partials -> lateral buffer (ring.cuh layout): a ring row (j = 0 or
+      // P) stores all P+1 of its nodes as one 16-byte pair per lane
+      const bool rowring = G == 0 || G == P;
+      if (rowring)
+        *reinterpret_cast<double2*>(A.lateral + Lat.y_index(P, A.nx, Z, ey + (G == P), G == 0, ex, 2 * t)) =
+            make_double2(o[0], o[1]);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
+        const double uv = e ? u2.y : u2.x;
         const int i = 2 * t + e, X = ex * P + i;
-        const bool ring = i == 0 || i == P || G == 0 || G == P;
+        const bool ring = rowring || i == 0 || i == P;
         if (ring) {
-          A.lateral[Z * lat_stride + static_cast<long long>(col) * (4 * P) + ring_index(P, i, G)] = o[e];
+          if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[e];
+          if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
+            if (zbc || (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
+              if (ring_owner(P, i, G, ex, ey, A.nx, A.ny)) dot = fma(uv, uv, dot);  // w = u, counted once
+            } else {
+              dot = fma(uv, o[e], dot);
+            }
+          }
         } else {
           const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-          double v = o[e];
-          if (zbc) v = __ldg(A.u + node);
+          const double v = zbc ? uv : o[e];
           A.w[node] = v;
-          if (do_dot) dot = fma(__ldg(A.u + node), v, dot);
+          if (do_dot) dot = fma(uv, v, dot);
         }
       }
     }
     __syncthreads();
   }
+  double cdot = 0.0;
   if (do_dot) {
     double v = dot;
 #pragma unroll
@@ -399,12 +416,12 @@ __global__ void __launch_bounds__(NT, 2)
     if (lane == 0) s_red[warp] = v;
     __syncthreads();
     if (tid == 0) {
-      double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s += s_red[w];
-      A.col_dot[col] = s;
+      for (int w = 0; w < NW; ++w) cdot += s_red[w];
     }
+    __syncthreads();
   }
+  ring_dot_finish<NT>(A, col, cdot, s_red);
 }
 
 }  // namespace

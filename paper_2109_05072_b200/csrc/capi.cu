@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "ring.cuh"
 
 struct hexbp_setup_s {
   hxb::Setup s;
@@ -333,8 +334,12 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
     if (!e) e = cudaMemset(*p, 0, bytes);
   };
   w.fixup_grid = fixup_grid(s);
-  al(reinterpret_cast<void**>(&w.lateral),
-     sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * (static_cast<std::size_t>(s.dims[2]) * s.p + 1));
+  {
+    const std::size_t nz_nodes = static_cast<std::size_t>(s.dims[2]) * s.p + 1;
+    const std::size_t exact = static_cast<std::size_t>(ncols) * 4 * s.p * nz_nodes;
+    const std::size_t fast = static_cast<std::size_t>(lat_fast_doubles(s.p, s.dims[0], s.dims[1], nz_nodes));
+    al(reinterpret_cast<void**>(&w.lateral), sizeof(double) * (exact > fast ? exact : fast));
+  }
   al(reinterpret_cast<void**>(&w.zupper), sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * s.dims[2]);
   al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * ncols);
   al(reinterpret_cast<void**>(&w.fix_partials), sizeof(double) * w.fixup_grid);
@@ -360,7 +365,7 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   if (!wh) return;
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
-  void* bufs[] = {w.lateral, w.zupper, w.fix_partials, w.fix_done, w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
+  void* bufs[] = {w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
                   w.vec_done, w.history, w.dot_result};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -415,9 +420,9 @@ int hexbp_cg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, 
       CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, st));
       CK(launch_cg_pap(w, n, st));
     } else {
-      CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st));
+      CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
     }
-    CK(launch_cg_update_r(w, n, st));
+    CK(launch_cg_update_r(w, n, st, constrained));
     CK(launch_cg_update_xp(w, x, n, st));
     if (k % check_every == 0 && k < max_iter) {
       CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));

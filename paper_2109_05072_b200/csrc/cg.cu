@@ -25,6 +25,7 @@
 
 #include "device_util.cuh"
 #include "internal.h"
+#include "ring.cuh"
 
 namespace hxb {
 namespace {
@@ -269,33 +270,120 @@ __global__ void __launch_bounds__(VT) fused_init_kernel(const double* __restrict
   }
 }
 
-__global__ void __launch_bounds__(VT) fused_update_r_kernel(const double* __restrict__ Ap, double* __restrict__ r,
-                                                            long long n, double* part, unsigned int* done,
-                                                            DevScalars* sc, double* hist) {
+// FUSED mode, r = r - alpha A p with A p's ring nodes still as column
+// partials (launch_apply(..., finish_ring = false)): every ring node sums its
+// 1-4 partials in ascending column order (ring.cuh; the values equal the ones
+// lateral_fixup_kernel would store, bit for bit) where A p is consumed, so the
+// ring never makes a round trip through HBM as A p. One warp per node row
+// (Y, Z); four row segments of 32 nodes in flight per warp.
+struct RingUpdateArgs {
+  const double* Ap;       // final on interior nodes
+  const double* p;        // the applied vector (ConstrainedOperator rows: A p = p)
+  const double* latY;     // ring partials (ring.cuh layout)
+  const double* latX;
+  double* r;
+  int nx, ny, Nx, Ny, Nz, constrained, bc_zlo, bc_zhi;
+};
+
+template <int P>
+__global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_constant__ RingUpdateArgs R, double* part,
+                                                                 unsigned int* done, DevScalars* sc, double* hist) {
   __shared__ double red[VT / 32];
   if (*(volatile int*)&sc->status != ST_RUNNING) return;
   const double alpha = sc->alpha;
+  const int lane = threadIdx.x & 31;
+  const int rows = R.Ny * R.Nz;  // < 2^31 (n_L < 2^31 checked at setup)
+  const LatLayout L(P, R.nx, R.ny);
   double acc = 0.0;
-  const long long stride = static_cast<long long>(gridDim.x) * VT;
-  long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x;
-  for (; i + 3 * stride < n; i += 4 * stride) {
-    double av[4], rv[4];
+  const int lmod = lane % P;
+  for (int row = blockIdx.x * (VT / 32) + (threadIdx.x >> 5); row < rows; row += gridDim.x * (VT / 32)) {
+    const int Z = row / R.Ny, Y = row - Z * R.Ny;
+    const bool bcrow = R.constrained && (Y == 0 || Y == R.Ny - 1 || (Z == 0 && R.bc_zlo) || (Z == R.Nz - 1 && R.bc_zhi));
+    double* rr_ = R.r + static_cast<long long>(R.Nx) * row;
+    const double* ap = R.Ap + static_cast<long long>(R.Nx) * row;
+    const double* pp = R.p + static_cast<long long>(R.Nx) * row;
+    if (Y % P != 0) {
+      // plain row: interior nodes read A p; x-face nodes X = fx*P sum the
+      // (left, right) partial pair of latX (one 16-byte load)
+      const double* xr = R.latX + L.x_index(R.nx, Z, Y, 0, 0);
+      for (int x0 = 0; x0 < R.Nx; x0 += 4 * 32) {
+        double a[4], rv[4];
+        double2 lr[4];
+        int xm = (x0 % P + lmod) % P;  // X % P for u = 0
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      av[u] = Ap[i + u * stride];
-      rv[u] = r[i + u * stride];
-    }
+        for (int u = 0; u < 4; ++u) {
+          const int X = x0 + 32 * u + lane;
+          const bool ok = X < R.Nx;
+          const bool xface = ok && xm == 0;
+          const bool bc = xface && R.constrained && (bcrow || X == 0 || X == R.Nx - 1);
+          rv[u] = ok ? rr_[X] : 0.0;
+          a[u] = ok && !xface ? ap[X] : (bc ? pp[X] : 0.0);
+          lr[u] = xface && !bc ? __ldcg(reinterpret_cast<const double2*>(xr) + X / P) : make_double2(0.0, 0.0);
+          if (xface && !bc) {
+            const int fx = X / P;
+            double sum = 0.0;  // ascending column order (ring_node_sum)
+            if (fx > 0) sum += lr[u].x;
+            if (fx < R.nx) sum += lr[u].y;
+            a[u] = sum;
+          }
+          xm += 32 % P;
+          if (xm >= P) xm -= P;
+        }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double v = fma(-alpha, av[u], rv[u]);
-      r[i + u * stride] = v;
-      acc = fma(v, v, acc);
+        for (int u = 0; u < 4; ++u) {
+          const int X = x0 + 32 * u + lane;
+          if (X < R.Nx) {
+            const double v = fma(-alpha, a[u], rv[u]);
+            rr_[X] = v;
+            acc = fma(v, v, acc);
+          }
+        }
+      }
+    } else {
+      // ring row Y = fy*P: every node sums the latY partials of the columns
+      // below / above (and both x-columns at a corner), ascending column order
+      const int fy = Y / P;
+      const bool below = fy > 0, above = fy < R.ny;
+      const double* yb = R.latY + L.y_index(P, R.nx, Z, fy, 0, 0, 0);  // side 0 (column below)
+      const double* ya = yb + static_cast<long long>(R.nx) * (P + 1);   // side 1 (column above)
+      for (int x0 = 0; x0 < R.Nx; x0 += 2 * 32) {
+        double a[2], rv[2], q[2][4];
+        bool lo[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int X = x0 + 32 * u + lane;
+          const bool ok = X < R.Nx;
+          const bool bc = ok && R.constrained && (bcrow || X == 0 || X == R.Nx - 1);
+          const bool need = ok && !bc;
+          const int cxh = X / P < R.nx ? X / P : R.nx - 1;
+          const int o = cxh * (P + 1) + (X - cxh * P);  // (cxh, ih) in a side's [cx][i] block
+          lo[u] = X % P == 0 && X > 0 && X / P < R.nx;  // interior corner: (cxh-1, P) at o - 1
+          rv[u] = ok ? rr_[X] : 0.0;
+          a[u] = bc ? pp[X] : 0.0;
+          q[u][0] = need && below && lo[u] ? __ldcg(yb + o - 1) : 0.0;
+          q[u][1] = need && below ? __ldcg(yb + o) : 0.0;
+          q[u][2] = need && above && lo[u] ? __ldcg(ya + o - 1) : 0.0;
+          q[u][3] = need && above ? __ldcg(ya + o) : 0.0;
+          if (need) {
+            double sum = 0.0;
+            if (below && lo[u]) sum += q[u][0];
+            if (below) sum += q[u][1];
+            if (above && lo[u]) sum += q[u][2];
+            if (above) sum += q[u][3];
+            a[u] = sum;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int X = x0 + 32 * u + lane;
+          if (X < R.Nx) {
+            const double v = fma(-alpha, a[u], rv[u]);
+            rr_[X] = v;
+            acc = fma(v, v, acc);
+          }
+        }
+      }
     }
-  }
-  for (; i < n; i += stride) {
-    const double v = fma(-alpha, Ap[i], r[i]);
-    r[i] = v;
-    acc = fma(v, v, acc);
   }
   const double s = block_sum<VT>(acc, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -414,13 +502,44 @@ cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st) {
+cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained) {
   if (ws.exact) {
     blocked_reduce_kernel<OP_UPDATE_R><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
                                                                      ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
-  } else {
-    fused_update_r_kernel<<<vec_grid(n), VT, 0, st>>>(ws.Ap, ws.r, n, ws.vec_partials, ws.vec_done, ws.sc,
-                                                      ws.history);
+    return cudaGetLastError();
+  }
+  // fast mode: A p comes from launch_apply(..., finish_ring = false)
+  const Setup& s = *ws.s;
+  RingUpdateArgs R;
+  R.Ap = ws.Ap;
+  R.p = ws.p;
+  R.latY = ws.lateral;
+  R.latX = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
+  R.r = ws.r;
+  R.nx = s.dims[0];
+  R.ny = s.dims[1];
+  R.Nx = s.dims[0] * s.p + 1;
+  R.Ny = s.dims[1] * s.p + 1;
+  R.Nz = s.dims[2] * s.p + 1;
+  R.constrained = constrained;
+  R.bc_zlo = s.bc_zlo;
+  R.bc_zhi = s.bc_zhi;
+  const int grid = vec_grid(n);
+  switch (s.p) {
+#define HXB_RING_CASE(PP)                                                                                   \
+  case PP:                                                                                                   \
+    fused_ring_update_r_kernel<PP><<<grid, VT, 0, st>>>(R, ws.vec_partials, ws.vec_done, ws.sc, ws.history); \
+    break;
+    HXB_RING_CASE(1)
+    HXB_RING_CASE(2)
+    HXB_RING_CASE(3)
+    HXB_RING_CASE(4)
+    HXB_RING_CASE(5)
+    HXB_RING_CASE(6)
+    HXB_RING_CASE(7)
+    HXB_RING_CASE(8)
+#undef HXB_RING_CASE
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

@@ -80,6 +80,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 namespace hxb {
 
+// Barrier among a subset of the CTA's warps (id 1..15; id 0 is __syncthreads).
+__device__ __forceinline__ void named_barrier_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---- asynchronous copies into shared memory (TMA bulk engine / LDGSTS)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -50,7 +50,8 @@ struct ApplyArgs {
   int ncols;                // nx * ny
   int constrained;          // ConstrainedOperator semantics (solver.hpp:60-65)
   int bc_zlo, bc_zhi;       // z-faces that are essential (slab partitions)
-  double* lateral;          // ring partials [Z][column][4p]
+  double* lateral;          // ring partials: exact mode [Z][column][4p]; fast mode latY (ring.cuh)
+  double* lat_x;            // fast mode: latX (ring.cuh)
   double* zupper;           // exact mode: upper-layer ring partials of z-shared planes [ez][column][4p]
   double* col_dot;          // per-column partial p.Ap (nullptr: no dot)
   double* fix_partials;     // per-block partial p.Ap of the lateral fix-up
@@ -102,8 +103,10 @@ struct Workspace {
 };
 
 // ---- apply.cu
+// finish_ring = false leaves the ring nodes of w as lateral partials (CG fast
+// mode: launch_cg_update_r sums them).
 cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
-                         double* dot_out, DevScalars* sc, cudaStream_t st);
+                         double* dot_out, DevScalars* sc, cudaStream_t st, bool finish_ring = true);
 int fixup_grid(const Setup& s);
 // ---- apply_mma.cu (FP64 tensor-core kernel, BP3 p = 7)
 bool mma_kernel_applies(const Setup& s);
@@ -116,7 +119,7 @@ void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* 
 // ---- cg.cu
 cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
                            cudaStream_t st);
-cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st);
+cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained = 1);
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st);
 int64_t reduction_partials(int64_t n);
 cudaError_t launch_cgd_reduce(const Workspace& ws, int op, const double* b, int64_t n, int64_t owned, double* out,

@@ -26,6 +26,8 @@
 //       <-> a = 2t, 2t+1): no transpose between the two x contractions
 //   Y': 9 groups (c)             -> C1 = B_y^T A1 + D_y^T A2, C2 = B_y^T A3
 //   Z': 8 groups (j)             -> out = B_z^T C1 + D_z^T C2     -> scatter
+// The phases of consecutive elements are software-pipelined into two barrier
+// intervals per element (see the schedule at the end of the kernel).
 // Shared-memory layouts are [field][k][pencil] with strides / XOR swizzles
 // chosen so that the B-fragment loads (k = lane%4 (+4), pencil = lane/4) and
 // the 16-byte C-fragment stores are bank-conflict free.
@@ -61,17 +63,20 @@ __device__ __forceinline__ int swa(int row) { return (row & 2) << 1; }
 constexpr int SB_KS = 92;
 __device__ __forceinline__ int sbi(int k, int p) { return k * SB_KS + (p ^ (((k >> 2) & 1) << 2)); }
 constexpr int SB_F = N * SB_KS;           // 736
-constexpr int SC_KS = 68;                 // [f][c][i + 8j] (Y'->Z'), aliases SB
+constexpr int SC_KS = 68;                 // [f][c][i + 8j] (Y'->Z')
 constexpr int SC_F = Q * SC_KS;           // 612
-constexpr int OFF_SA = 0;
-constexpr int OFF_SB = OFF_SA + 3 * SA_F;
-constexpr int OFF_G = OFF_SB + 3 * SB_F;  // 16-byte aligned (even)
+constexpr int NUB = 4;                    // u staging buffers: U(e-1) .. U(e+2) live at once
+constexpr int OFF_SA = 0;                 // Z -> Y   : 2 fields, SA layout
+constexpr int OFF_SP = OFF_SA + 2 * SA_F;  // X' -> Y' : 3 fields, SA layout
+constexpr int OFF_SB = OFF_SP + 3 * SA_F;  // Y -> X   : 3 fields
+constexpr int OFF_SC = OFF_SB + 3 * SB_F;  // Y' -> Z' : 2 fields
+constexpr int OFF_G = OFF_SC + 2 * SC_F;   // 16-byte aligned (even)
 constexpr int OFF_U = OFF_G + GSE;
-constexpr int OFF_BAS = OFF_U + 2 * US_SZ;  // B, D (q x n each), resident
+constexpr int OFF_BAS = OFF_U + NUB * US_SZ;  // B, D (q x n each), resident
 constexpr int OFF_BAR = OFF_BAS + 2 * Q * N;
 constexpr int SMEM_BYTES = (OFF_BAR + 1) * 8;
 static_assert(OFF_G % 2 == 0, "TMA destination must be 16-byte aligned");
-static_assert(3 * SB_F >= 2 * SC_F, "SC aliases SB");
+static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "two CTAs per SM");
 
 struct MmaBasis {
   double B[Q][N];
@@ -101,8 +106,9 @@ __global__ void __launch_bounds__(NT, 2)
     bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs) {
   extern __shared__ double smem[];
   double* SA = smem + OFF_SA;
+  double* SP = smem + OFF_SP;
   double* SB = smem + OFF_SB;
-  double* SC = SB;  // phase Y' -> Z' (SB is consumed in phase X)
+  double* SC = smem + OFF_SC;
   double* Gs = smem + OFF_G;
   double* Us = smem + OFF_U;
   __shared__ double s_red[NW];
@@ -115,9 +121,9 @@ __global__ void __launch_bounds__(NT, 2)
   const bool do_dot = A.col_dot != nullptr;
   const int col = blockIdx.x;
   const int ex = col % A.nx, ey = col / A.nx;
+  const int nz = A.nz;
   const LatLayout Lat(P, A.nx, A.ny);
 
-  // basis fragments, resident for the whole kernel
   // Basis: B and D stay in shared memory for the whole kernel. The 8 x 8
   // MMA fragments are read once into registers with volatile loads (read from
   // the parameter bank with a lane-dependent index, ptxas would re-issue
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(NT, 2)
   const double* rB = sB + 8 * N;  // row a = 8
   const double* rD = sD + 8 * N;
 
-  const double* Gcol = A.G + static_cast<long long>(col) * A.nz * GSE;
+  const double* Gcol = A.G + static_cast<long long>(col) * nz * GSE;
   constexpr uint32_t gbytes = GSE * 8;
   const uint32_t bar = smem_u32(smem + OFF_BAR);
   if (tid == 0) {
@@ -152,260 +158,288 @@ __global__ void __launch_bounds__(NT, 2)
   if (tid == 0) {
     mbar_arrive_expect_tx(bar, gbytes);
     bulk_g2s(smem_u32(Gs), Gcol, gbytes, bar, pol);
-    if (A.nz > 1) prefetch_l2_bulk(Gcol + GSE, gbytes);
+    if (nz > 1) prefetch_l2_bulk(Gcol + GSE, gbytes);
   }
-  // u staging: thread (i,j) of the footprint (tid < 64) copies its z-pencil into [k][j*8+i]
-  auto fetch_u = [&](int ez, int buf) {
-    if (tid < N * N) {
+  // u staging of element e into buffer e % NUB: thread (i,j) of the footprint
+  // (tid < 64) copies its z-pencil into [k][j*8+i]
+  auto fetch_u = [&](int e) {
+    if (e < nz && tid < N * N) {
       const int i = tid & 7, j = tid >> 3;
-      const uint32_t dst = smem_u32(Us + buf * US_SZ + tid);
+      const uint32_t dst = smem_u32(Us + (e % NUB) * US_SZ + tid);
       const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
       const long long plane = static_cast<long long>(A.Nx) * A.Ny;
 #pragma unroll
-      for (int k = 0; k < N; ++k) cp_async8(dst + k * US_KS * 8, A.u + base + plane * (ez * P + k));
+      for (int k = 0; k < N; ++k) cp_async8(dst + k * US_KS * 8, A.u + base + plane * (e * P + k));
     }
     cp_async_commit();
   };
-  fetch_u(0, 0);
 
-  double carry[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // z-carry of the two j-groups this warp owns
-  double dot = 0.0;
-
-  for (int ez = 0; ez < A.nz; ++ez) {
-    if (tid == 0 && ez + 2 < A.nz) prefetch_l2_bulk(Gcol + (ez + 2) * GSE, gbytes);
-    if (ez + 1 < A.nz) {
-      fetch_u(ez + 1, (ez + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* us = Us + (ez & 1) * US_SZ;
-
-    // ------------------------------------------------ phase Z
-    for (int G = warp; G < N; G += NW) {  // G = j; pencil i = g
-      const int X = ex * P + g, Y = ey * P + G;
-      const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
-      double b[2];
+  // ------------------------------------------------ phase bodies
+  // Z(e, j): z contraction of element e, pencil group j (i = g) -> SA
+  auto phaseZ = [&](int e, int G) {
+    const double* us = Us + (e % NUB) * US_SZ;
+    const int X = ex * P + g, Y = ey * P + G;
+    const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+    double b[2];
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int k = t + 4 * s, Z = ez * P + k;
-        double v = us[k * US_KS + G * 8 + g];
-        if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
-        b[s] = v;
-      }
-      double cb0 = 0, cb1 = 0, cd0 = 0, cd1 = 0;
-      dmma(cb0, cb1, aB0, b[0]);
-      dmma(cb0, cb1, aB1, b[1]);
-      dmma(cd0, cd1, aD0, b[0]);
-      dmma(cd0, cd1, aD1, b[1]);
-      const double r8b = quad_sum(fma(rB[t + 4], b[1], rB[t] * b[0]));
-      const double r8d = quad_sum(fma(rD[t + 4], b[1], rD[t] * b[0]));
-      // SA[f][j = G][8 a3 + i]: rows a3 = g, cols i = 2t, 2t+1; row a3 = 8 at i = g
-      double* sa = SA + G * SA_KS;
-      const int h = swa(G);
-      *reinterpret_cast<double2*>(sa + 8 * g + (2 * t ^ h)) = make_double2(cb0, cb1);
-      *reinterpret_cast<double2*>(sa + SA_F + 8 * g + (2 * t ^ h)) = make_double2(cd0, cd1);
-      if (t == 0) {
-        sa[64 + (g ^ h)] = r8b;
-        sa[SA_F + 64 + (g ^ h)] = r8d;
-      }
+    for (int s = 0; s < 2; ++s) {
+      const int k = t + 4 * s, Z = e * P + k;
+      double v = us[k * US_KS + G * 8 + g];
+      if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
+      b[s] = v;
     }
-    __syncthreads();
+    double cb0 = 0, cb1 = 0, cd0 = 0, cd1 = 0;
+    dmma(cb0, cb1, aB0, b[0]);
+    dmma(cb0, cb1, aB1, b[1]);
+    dmma(cd0, cd1, aD0, b[0]);
+    dmma(cd0, cd1, aD1, b[1]);
+    const double r8b = quad_sum(fma(rB[t + 4], b[1], rB[t] * b[0]));
+    const double r8d = quad_sum(fma(rD[t + 4], b[1], rD[t] * b[0]));
+    // SA[f][j = G][8 a3 + i]: rows a3 = g, cols i = 2t, 2t+1; row a3 = 8 at i = g
+    double* sa = SA + G * SA_KS;
+    const int h = swa(G);
+    *reinterpret_cast<double2*>(sa + 8 * g + (2 * t ^ h)) = make_double2(cb0, cb1);
+    *reinterpret_cast<double2*>(sa + SA_F + 8 * g + (2 * t ^ h)) = make_double2(cd0, cd1);
+    if (t == 0) {
+      sa[64 + (g ^ h)] = r8b;
+      sa[SA_F + 64 + (g ^ h)] = r8d;
+    }
+  };
 
-    // ------------------------------------------------ phase Y
-    for (int G = warp; G < Q; G += NW) {  // G = c; pencil i = g
-      const double* sa = SA + 8 * G + (g ^ swa(t));  // rows j = t, t+4 share the swizzle
-      const double x00 = sa[t * SA_KS], x01 = sa[(t + 4) * SA_KS];
-      const double x10 = sa[SA_F + t * SA_KS], x11 = sa[SA_F + (t + 4) * SA_KS];
-      double bb0 = 0, bb1 = 0, db0 = 0, db1 = 0, bd0 = 0, bd1 = 0;
-      dmma(bb0, bb1, aB0, x00);
-      dmma(bb0, bb1, aB1, x01);
-      dmma(db0, db1, aD0, x00);
-      dmma(db0, db1, aD1, x01);
-      dmma(bd0, bd1, aB0, x10);
-      dmma(bd0, bd1, aB1, x11);
-      const double r8bb = quad_sum(fma(rB[t + 4], x01, rB[t] * x00));
-      const double r8db = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));
-      const double r8bd = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
-      // SB[f][k = i][p = b + 9c]; rows b = g, cols i = 2t, 2t+1
-      const int i0 = sbi(2 * t, g + 9 * G), i1 = sbi(2 * t + 1, g + 9 * G);
-      SB[i0] = bb0;
-      SB[i1] = bb1;
-      SB[SB_F + i0] = db0;
-      SB[SB_F + i1] = db1;
-      SB[2 * SB_F + i0] = bd0;
-      SB[2 * SB_F + i1] = bd1;
-      if (t == 0) {  // b = 8, k = i = g
-        const int i8 = sbi(g, 8 + 9 * G);
-        SB[i8] = r8bb;
-        SB[SB_F + i8] = r8db;
-        SB[2 * SB_F + i8] = r8bd;
-      }
+  // Y(c): y contraction, a3 group c (pencil i = g) -> SB
+  auto phaseY = [&](int G) {
+    const double* sa = SA + 8 * G + (g ^ swa(t));  // rows j = t, t+4 share the swizzle
+    const double x00 = sa[t * SA_KS], x01 = sa[(t + 4) * SA_KS];
+    const double x10 = sa[SA_F + t * SA_KS], x11 = sa[SA_F + (t + 4) * SA_KS];
+    double bb0 = 0, bb1 = 0, db0 = 0, db1 = 0, bd0 = 0, bd1 = 0;
+    dmma(bb0, bb1, aB0, x00);
+    dmma(bb0, bb1, aB1, x01);
+    dmma(db0, db1, aD0, x00);
+    dmma(db0, db1, aD1, x01);
+    dmma(bd0, bd1, aB0, x10);
+    dmma(bd0, bd1, aB1, x11);
+    const double r8bb = quad_sum(fma(rB[t + 4], x01, rB[t] * x00));
+    const double r8db = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));
+    const double r8bd = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
+    // SB[f][k = i][p = b + 9c]; rows b = g, cols i = 2t, 2t+1
+    const int i0 = sbi(2 * t, g + 9 * G), i1 = sbi(2 * t + 1, g + 9 * G);
+    SB[i0] = bb0;
+    SB[i1] = bb1;
+    SB[SB_F + i0] = db0;
+    SB[SB_F + i1] = db1;
+    SB[2 * SB_F + i0] = bd0;
+    SB[2 * SB_F + i1] = bd1;
+    if (t == 0) {  // b = 8, k = i = g
+      const int i8 = sbi(g, 8 + 9 * G);
+      SB[i8] = r8bb;
+      SB[SB_F + i8] = r8db;
+      SB[2 * SB_F + i8] = r8bd;
     }
-    __syncthreads();
+  };
 
-    // ------------------------------------------------ phase X
-    // Transposed MMA form: C^T[pencil][a] = sum_i X^T[pencil][i] M^T[i][a], so
-    // lane (g, t) ends with pencil g at points a = 2t, 2t+1 -- exactly the
-    // A-fragment (row g, k-slot t <-> a = 2t / 2t+1) of the backward MMA. No
-    // transpose between the forward and backward x contractions.
-    mbar_wait_parity(bar, ez & 1);
-    for (int G = warp; G < 11; G += NW) {  // pencils p = 8G + g over (b, c), valid p < 81
-      const int k0 = sbi(t, 8 * G + g), k1 = sbi(t + 4, 8 * G + g);
-      const double x00 = SB[k0], x01 = SB[k1];
-      const double x10 = SB[SB_F + k0], x11 = SB[SB_F + k1];
-      const double x20 = SB[2 * SB_F + k0], x21 = SB[2 * SB_F + k1];
-      double gr[2] = {0, 0}, gs[2] = {0, 0}, gt[2] = {0, 0};
-      dmma(gr[0], gr[1], x00, aD0);
-      dmma(gr[0], gr[1], x01, aD1);
-      dmma(gs[0], gs[1], x10, aB0);
-      dmma(gs[0], gs[1], x11, aB1);
-      dmma(gt[0], gt[1], x20, aB0);
-      dmma(gt[0], gt[1], x21, aB1);
-      double r8r = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));  // a = 8 of pencil g (all 4 lanes)
-      double r8s = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
-      double r8t = quad_sum(fma(rB[t + 4], x21, rB[t] * x20));
-      const int p = 8 * G + g;
-      if (p < QQ) {
-        // pointwise factors (operator.hpp:129-131); [qp][6] layout, qp = a + 9p:
-        // points a = 2t, 2t+1 are 12 contiguous doubles (conflict-free 16-byte loads)
-        const double2* gp = reinterpret_cast<const double2*>(Gs + (2 * t + Q * p) * 6);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double2 ga = gp[3 * e], gb = gp[3 * e + 1], gc = gp[3 * e + 2];
-          const double r = gr[e], s_ = gs[e], u = gt[e];
-          gr[e] = ga.x * r + ga.y * s_ + gb.x * u;
-          gs[e] = ga.y * r + gb.y * s_ + gc.x * u;
-          gt[e] = gb.x * r + gc.x * s_ + gc.y * u;
-        }
-        const double2* g8 = reinterpret_cast<const double2*>(Gs + (8 + Q * p) * 6);
-        const double2 ga = g8[0], gb = g8[1], gc = g8[2];
-        const double r = r8r, s_ = r8s, u = r8t;
-        r8r = ga.x * r + ga.y * s_ + gb.x * u;
-        r8s = ga.y * r + gb.y * s_ + gc.x * u;
-        r8t = gb.x * r + gc.x * s_ + gc.y * u;
-      }
-      // backward: W[p][i] = sum_a A[p][a] M[a][i]; a = 8 term first
-      double w1[2], w2[2], w3[2];
-      w1[0] = rD[2 * t] * r8r;
-      w1[1] = rD[2 * t + 1] * r8r;
-      w2[0] = rB[2 * t] * r8s;
-      w2[1] = rB[2 * t + 1] * r8s;
-      w3[0] = rB[2 * t] * r8t;
-      w3[1] = rB[2 * t + 1] * r8t;
-      dmma(w1[0], w1[1], gr[0], eD0);
-      dmma(w1[0], w1[1], gr[1], eD1);
-      dmma(w2[0], w2[1], gs[0], eB0);
-      dmma(w2[0], w2[1], gs[1], eB1);
-      dmma(w3[0], w3[1], gt[0], eB0);
-      dmma(w3[0], w3[1], gt[1], eB1);
-      // pencil p = b + 9c, outputs i = 2t, 2t+1 -> SA[f][b][8c + i] (16-byte stores)
-      if (p < QQ) {
-        const int c = p / 9, bq = p - 9 * c;
-        double* d = SA + bq * SA_KS + 8 * c + (2 * t ^ swa(bq));
-        *reinterpret_cast<double2*>(d) = make_double2(w1[0], w1[1]);
-        *reinterpret_cast<double2*>(d + SA_F) = make_double2(w2[0], w2[1]);
-        *reinterpret_cast<double2*>(d + 2 * SA_F) = make_double2(w3[0], w3[1]);
-      }
-    }
-    __syncthreads();
-    if (tid == 0 && ez + 1 < A.nz) {  // G buffer consumed: stream the next element's block
-      fence_proxy_async();
-      mbar_arrive_expect_tx(bar, gbytes);
-      bulk_g2s(smem_u32(Gs), Gcol + (ez + 1) * GSE, gbytes, bar, pol);
-    }
-
-    // ------------------------------------------------ phase Y'
-    for (int G = warp; G < Q; G += NW) {  // G = c; pencil i = g; contraction over b
-      const double* sa = SA + 8 * G + (g ^ swa(t));
-      const double y00 = sa[t * SA_KS], y01 = sa[(t + 4) * SA_KS];
-      const double y10 = sa[SA_F + t * SA_KS], y11 = sa[SA_F + (t + 4) * SA_KS];
-      const double y20 = sa[2 * SA_F + t * SA_KS], y21 = sa[2 * SA_F + (t + 4) * SA_KS];
-      const double* s8 = SA + 8 * SA_KS + 8 * G + 2 * t;  // b = 8, pencils i = 2t, 2t+1
-      const double2 e1 = *reinterpret_cast<const double2*>(s8);
-      const double2 e2 = *reinterpret_cast<const double2*>(s8 + SA_F);
-      const double2 e3 = *reinterpret_cast<const double2*>(s8 + 2 * SA_F);
-      double c1[2], c2[2];
-      c1[0] = fma(rD[g], e2.x, rB[g] * e1.x);
-      c1[1] = fma(rD[g], e2.y, rB[g] * e1.y);
-      c2[0] = rB[g] * e3.x;
-      c2[1] = rB[g] * e3.y;
-      dmma(c1[0], c1[1], tB0, y00);
-      dmma(c1[0], c1[1], tB1, y01);
-      dmma(c1[0], c1[1], tD0, y10);
-      dmma(c1[0], c1[1], tD1, y11);
-      dmma(c2[0], c2[1], tB0, y20);
-      dmma(c2[0], c2[1], tB1, y21);
-      // rows j = g, cols i = 2t, 2t+1, c = G -> SC[f][c][i + 8j]
-      double* sc = SC + G * SC_KS + 8 * g + 2 * t;
-      *reinterpret_cast<double2*>(sc) = make_double2(c1[0], c1[1]);
-      *reinterpret_cast<double2*>(sc + SC_F) = make_double2(c2[0], c2[1]);
-    }
-    __syncthreads();
-
-    // ------------------------------------------------ phase Z' + transpose restriction (part 1)
-#pragma unroll
-    for (int slot = 0; slot < (N + NW - 1) / NW; ++slot) {  // G = j; pencil i = g; contraction over c
-      const int G = warp + NW * slot;
-      if (G >= N) break;  // warp-uniform
-      const double* sc = SC + 8 * G + g;
-      const double z00 = sc[t * SC_KS], z01 = sc[(t + 4) * SC_KS];
-      const double z10 = sc[SC_F + t * SC_KS], z11 = sc[SC_F + (t + 4) * SC_KS];
-      const double* s8 = SC + 8 * SC_KS + 8 * G + 2 * t;  // c = 8
-      const double2 e1 = *reinterpret_cast<const double2*>(s8);
-      const double2 e2 = *reinterpret_cast<const double2*>(s8 + SC_F);
-      double o[2];
-      o[0] = fma(rD[g], e2.x, rB[g] * e1.x);
-      o[1] = fma(rD[g], e2.y, rB[g] * e1.y);
-      dmma(o[0], o[1], tB0, z00);
-      dmma(o[0], o[1], tB1, z01);
-      dmma(o[0], o[1], tD0, z10);
-      dmma(o[0], o[1], tD1, z11);
-      // rows k = g (z node), cols i = 2t, 2t+1, j = G
-      const double top0 = __shfl_sync(0xffffffffu, carry[slot][0], 28 + t);
-      const double top1 = __shfl_sync(0xffffffffu, carry[slot][1], 28 + t);
-      if (g == 0) {
-        o[0] += top0;
-        o[1] += top1;
-      }
-      if (g == P && ez + 1 < A.nz) {
-        carry[slot][0] = o[0];
-        carry[slot][1] = o[1];
-        continue;
-      }
-      const int Z = ez * P + g, Y = ey * P + G;
-      const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
-      // u at these nodes: still staged in shared memory (z-plane k = g of this element)
-      const double2 u2 = *reinterpret_cast<const double2*>(us + g * US_KS + G * 8 + 2 * t);
-      // ring partials -> lateral buffer (ring.cuh layout): a ring row (j = 0 or
-      // P) stores all P+1 of its nodes as one 16-byte pair per lane
-      const bool rowring = G == 0 || G == P;
-      if (rowring)
-        *reinterpret_cast<double2*>(A.lateral + Lat.y_index(P, A.nx, Z, ey + (G == P), G == 0, ex, 2 * t)) =
-            make_double2(o[0], o[1]);
+  // X(G): x contraction forward, pointwise G, x contraction backward for the
+  // pencils p = 8G + g over (b, c) (valid p < 81) -> SP.
+  // Transposed MMA form: C^T[pencil][a] = sum_i X^T[pencil][i] M^T[i][a], so
+  // lane (g, t) ends with pencil g at points a = 2t, 2t+1 -- exactly the
+  // A-fragment (row g, k-slot t <-> a = 2t / 2t+1) of the backward MMA. No
+  // transpose between the forward and backward x contractions.
+  auto phaseX = [&](int G) {
+    const int k0 = sbi(t, 8 * G + g), k1 = sbi(t + 4, 8 * G + g);
+    const double x00 = SB[k0], x01 = SB[k1];
+    const double x10 = SB[SB_F + k0], x11 = SB[SB_F + k1];
+    const double x20 = SB[2 * SB_F + k0], x21 = SB[2 * SB_F + k1];
+    double gr[2] = {0, 0}, gs[2] = {0, 0}, gt[2] = {0, 0};
+    dmma(gr[0], gr[1], x00, aD0);
+    dmma(gr[0], gr[1], x01, aD1);
+    dmma(gs[0], gs[1], x10, aB0);
+    dmma(gs[0], gs[1], x11, aB1);
+    dmma(gt[0], gt[1], x20, aB0);
+    dmma(gt[0], gt[1], x21, aB1);
+    double r8r = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));  // a = 8 of pencil g (all 4 lanes)
+    double r8s = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
+    double r8t = quad_sum(fma(rB[t + 4], x21, rB[t] * x20));
+    const int p = 8 * G + g;
+    if (p < QQ) {
+      // pointwise factors (operator.hpp:129-131); [qp][6] layout, qp = a + 9p:
+      // points a = 2t, 2t+1 are 12 contiguous doubles (conflict-free 16-byte loads)
+      const double2* gp = reinterpret_cast<const double2*>(Gs + (2 * t + Q * p) * 6);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const double uv = e ? u2.y : u2.x;
-        const int i = 2 * t + e, X = ex * P + i;
-        const bool ring = rowring || i == 0 || i == P;
-        if (ring) {
-          if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[e];
-          if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
-            if (zbc || (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
-              if (ring_owner(P, i, G, ex, ey, A.nx, A.ny)) dot = fma(uv, uv, dot);  // w = u, counted once
-            } else {
-              dot = fma(uv, o[e], dot);
-            }
+        const double2 ga = gp[3 * e], gb = gp[3 * e + 1], gc = gp[3 * e + 2];
+        const double r = gr[e], s_ = gs[e], u = gt[e];
+        gr[e] = ga.x * r + ga.y * s_ + gb.x * u;
+        gs[e] = ga.y * r + gb.y * s_ + gc.x * u;
+        gt[e] = gb.x * r + gc.x * s_ + gc.y * u;
+      }
+      const double2* g8 = reinterpret_cast<const double2*>(Gs + (8 + Q * p) * 6);
+      const double2 ga = g8[0], gb = g8[1], gc = g8[2];
+      const double r = r8r, s_ = r8s, u = r8t;
+      r8r = ga.x * r + ga.y * s_ + gb.x * u;
+      r8s = ga.y * r + gb.y * s_ + gc.x * u;
+      r8t = gb.x * r + gc.x * s_ + gc.y * u;
+    }
+    // backward: W[p][i] = sum_a A[p][a] M[a][i]; a = 8 term first
+    double w1[2], w2[2], w3[2];
+    w1[0] = rD[2 * t] * r8r;
+    w1[1] = rD[2 * t + 1] * r8r;
+    w2[0] = rB[2 * t] * r8s;
+    w2[1] = rB[2 * t + 1] * r8s;
+    w3[0] = rB[2 * t] * r8t;
+    w3[1] = rB[2 * t + 1] * r8t;
+    dmma(w1[0], w1[1], gr[0], eD0);
+    dmma(w1[0], w1[1], gr[1], eD1);
+    dmma(w2[0], w2[1], gs[0], eB0);
+    dmma(w2[0], w2[1], gs[1], eB1);
+    dmma(w3[0], w3[1], gt[0], eB0);
+    dmma(w3[0], w3[1], gt[1], eB1);
+    // pencil p = b + 9c, outputs i = 2t, 2t+1 -> SP[f][b][8c + i] (16-byte stores)
+    if (p < QQ) {
+      const int c = p / 9, bq = p - 9 * c;
+      double* d = SP + bq * SA_KS + 8 * c + (2 * t ^ swa(bq));
+      *reinterpret_cast<double2*>(d) = make_double2(w1[0], w1[1]);
+      *reinterpret_cast<double2*>(d + SA_F) = make_double2(w2[0], w2[1]);
+      *reinterpret_cast<double2*>(d + 2 * SA_F) = make_double2(w3[0], w3[1]);
+    }
+  };
+
+  // Y'(c): y contraction backward, a3 group c (pencil i = g; over b) -> SC
+  auto phaseYp = [&](int G) {
+    const double* sa = SP + 8 * G + (g ^ swa(t));
+    const double y00 = sa[t * SA_KS], y01 = sa[(t + 4) * SA_KS];
+    const double y10 = sa[SA_F + t * SA_KS], y11 = sa[SA_F + (t + 4) * SA_KS];
+    const double y20 = sa[2 * SA_F + t * SA_KS], y21 = sa[2 * SA_F + (t + 4) * SA_KS];
+    const double* s8 = SP + 8 * SA_KS + 8 * G + 2 * t;  // b = 8, pencils i = 2t, 2t+1
+    const double2 e1 = *reinterpret_cast<const double2*>(s8);
+    const double2 e2 = *reinterpret_cast<const double2*>(s8 + SA_F);
+    const double2 e3 = *reinterpret_cast<const double2*>(s8 + 2 * SA_F);
+    double c1[2], c2[2];
+    c1[0] = fma(rD[g], e2.x, rB[g] * e1.x);
+    c1[1] = fma(rD[g], e2.y, rB[g] * e1.y);
+    c2[0] = rB[g] * e3.x;
+    c2[1] = rB[g] * e3.y;
+    dmma(c1[0], c1[1], tB0, y00);
+    dmma(c1[0], c1[1], tB1, y01);
+    dmma(c1[0], c1[1], tD0, y10);
+    dmma(c1[0], c1[1], tD1, y11);
+    dmma(c2[0], c2[1], tB0, y20);
+    dmma(c2[0], c2[1], tB1, y21);
+    // rows j = g, cols i = 2t, 2t+1, c = G -> SC[f][c][i + 8j]
+    double* sc = SC + G * SC_KS + 8 * g + 2 * t;
+    *reinterpret_cast<double2*>(sc) = make_double2(c1[0], c1[1]);
+    *reinterpret_cast<double2*>(sc + SC_F) = make_double2(c2[0], c2[1]);
+  };
+
+  // Z'(e, j) + transpose restriction part 1: z contraction backward of
+  // element e, j group (pencil i = g); z-shared plane carried in registers
+  // (this warp always owns group j).
+  double carry[2] = {0.0, 0.0};
+  double dot = 0.0;
+  auto phaseZp = [&](int e, int G) {
+    const double* sc = SC + 8 * G + g;
+    const double z00 = sc[t * SC_KS], z01 = sc[(t + 4) * SC_KS];
+    const double z10 = sc[SC_F + t * SC_KS], z11 = sc[SC_F + (t + 4) * SC_KS];
+    const double* s8 = SC + 8 * SC_KS + 8 * G + 2 * t;  // c = 8
+    const double2 e1 = *reinterpret_cast<const double2*>(s8);
+    const double2 e2 = *reinterpret_cast<const double2*>(s8 + SC_F);
+    double o[2];
+    o[0] = fma(rD[g], e2.x, rB[g] * e1.x);
+    o[1] = fma(rD[g], e2.y, rB[g] * e1.y);
+    dmma(o[0], o[1], tB0, z00);
+    dmma(o[0], o[1], tB1, z01);
+    dmma(o[0], o[1], tD0, z10);
+    dmma(o[0], o[1], tD1, z11);
+    // rows k = g (z node), cols i = 2t, 2t+1, j = G
+    const double top0 = __shfl_sync(0xffffffffu, carry[0], 28 + t);
+    const double top1 = __shfl_sync(0xffffffffu, carry[1], 28 + t);
+    if (g == 0) {
+      o[0] += top0;
+      o[1] += top1;
+    }
+    if (g == P && e + 1 < nz) {
+      carry[0] = o[0];
+      carry[1] = o[1];
+      return;
+    }
+    const int Z = e * P + g, Y = ey * P + G;
+    const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+    // u at these nodes: still staged in shared memory (z-plane k = g of element e)
+    const double2 u2 = *reinterpret_cast<const double2*>(Us + (e % NUB) * US_SZ + g * US_KS + G * 8 + 2 * t);
+    // ring partials -> lateral buffer (ring.cuh layout): a ring row (j = 0 or
+    // P) stores all P+1 of its nodes as one 16-byte pair per lane
+    const bool rowring = G == 0 || G == P;
+    if (rowring)
+      *reinterpret_cast<double2*>(A.lateral + Lat.y_index(P, A.nx, Z, ey + (G == P), G == 0, ex, 2 * t)) =
+          make_double2(o[0], o[1]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double uv = q ? u2.y : u2.x;
+      const int i = 2 * t + q, X = ex * P + i;
+      const bool ring = rowring || i == 0 || i == P;
+      if (ring) {
+        if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
+        if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
+          if (zbc || (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
+            if (ring_owner(P, i, G, ex, ey, A.nx, A.ny)) dot = fma(uv, uv, dot);  // w = u, counted once
+          } else {
+            dot = fma(uv, o[q], dot);
           }
-        } else {
-          const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-          const double v = zbc ? uv : o[e];
-          A.w[node] = v;
-          if (do_dot) dot = fma(uv, v, dot);
         }
+      } else {
+        const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+        const double v = zbc ? uv : o[q];
+        A.w[node] = v;
+        if (do_dot) dot = fma(uv, v, dot);
       }
     }
+  };
+
+  // ------------------------------------------------ skewed schedule
+  // Two barrier intervals per element, each mixing independent work of
+  // neighbouring elements so that no warp idles through a phase:
+  //   A_e : X(e) [warp = pencil group], Z(e+1), Z'(e-1)      -> SP, SA, w
+  //   B_e : Y'(e), Y(e+1)                                    -> SC, SB
+  // Buffers: SA (Z->Y), SP (X'->Y'), SB (Y->X), SC (Y'->Z') are each written
+  // and read in consecutive intervals; G(e+1) streams into the single G buffer
+  // during B_e (TMA, mbarrier); u of element e+2 is staged (cp.async) during
+  // A_e and B_e into one of NUB = 4 buffers (Z'(e-1) still reads u(e-1) for
+  // the p.Ap dot).
+  // Work map: Z'(j) on warp j (its carry registers), Z(j) on warp (j+8) % 11,
+  // Y'(c) on warp c, Y(c) on warp (c+9) % 11.
+  fetch_u(0);
+  fetch_u(1);
+  cp_async_wait<0>();
+  __syncthreads();
+  if (warp < N) phaseZ(0, warp);
+  __syncthreads();
+  if (warp < Q) phaseY(warp);
+  __syncthreads();
+  for (int e = 0; e <= nz; ++e) {
+    // ---- interval A_e
+    fetch_u(e + 2);
+    if (tid == 0 && e + 2 < nz) prefetch_l2_bulk(Gcol + (e + 2) * GSE, gbytes);
+    if (e < nz) {
+      mbar_wait_parity(bar, e & 1);
+      phaseX(warp);
+    }
+    if (e >= 1 && warp < N) phaseZp(e - 1, warp);
+    if (e + 1 < nz) {
+      const int j = warp >= 8 ? warp - 8 : warp + 3;  // inverse of (j + 8) % 11
+      if (j < N) phaseZ(e + 1, j);
+    }
+    if (e == nz) break;
+    __syncthreads();
+    // ---- interval B_e
+    if (tid == 0 && e + 1 < nz) {  // X(e) consumed the G buffer: stream G(e+1)
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, gbytes);
+      bulk_g2s(smem_u32(Gs), Gcol + (e + 1) * GSE, gbytes, bar, pol);
+    }
+    if (warp < Q) phaseYp(warp);
+    if (e + 1 < nz) {
+      const int c = warp >= 9 ? warp - 9 : warp + 2;  // inverse of (c + 9) % 11
+      if (c < Q) phaseY(c);
+    }
+    cp_async_wait<0>();  // u(e+2), issued at the top of A_e, is read by Z(e+2) in A_{e+1}
     __syncthreads();
   }
   double cdot = 0.0;

@@ -73,7 +73,8 @@ constexpr int OFF_SC = OFF_SB + 3 * SB_F;  // Y' -> Z' : 2 fields
 constexpr int OFF_G = OFF_SC + 2 * SC_F;   // 16-byte aligned (even)
 constexpr int OFF_U = OFF_G + GSE;
 constexpr int OFF_BAS = OFF_U + NUB * US_SZ;  // B, D (q x n each), resident
-constexpr int OFF_BAR = OFF_BAS + 2 * Q * N;
+constexpr int OFF_R8 = OFF_BAS + 2 * Q * N;   // packed row-8 pairs (16-byte loads)
+constexpr int OFF_BAR = OFF_R8 + 16 + 16;
 constexpr int SMEM_BYTES = (OFF_BAR + 1) * 8;
 static_assert(OFF_G % 2 == 0, "TMA destination must be 16-byte aligned");
 static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "two CTAs per SM");
@@ -146,6 +147,31 @@ __global__ void __launch_bounds__(NT, 2)
   const double eD0 = bas(sD, 2 * t, g), eD1 = bas(sD, 2 * t + 1, g);
   const double* rB = sB + 8 * N;  // row a = 8
   const double* rD = sD + 8 * N;
+  // row 8 packed for 16-byte loads: R8[t] = (B8[t], B8[t+4], D8[t], D8[t+4]),
+  // C8[g] = (B8[g], D8[g])
+  double* R8 = smem + OFF_R8;
+  if (tid < 4) {
+    R8[4 * tid] = rB[tid];
+    R8[4 * tid + 1] = rB[tid + 4];
+    R8[4 * tid + 2] = rD[tid];
+    R8[4 * tid + 3] = rD[tid + 4];
+  } else if (tid < 12) {
+    R8[16 + 2 * (tid - 4)] = rB[tid - 4];
+    R8[16 + 2 * (tid - 4) + 1] = rD[tid - 4];
+  }
+  __syncthreads();
+  // quad-sum partial of row 8 for fields M = B (0) or D (1) over k = t, t+4
+  auto row8B = [&](double x0, double x1) {
+    const double2 b = *reinterpret_cast<const double2*>(R8 + 4 * t);
+    return fma(b.y, x1, b.x * x0);
+  };
+  auto row8D = [&](double x0, double x1) {
+    const double2 d = *reinterpret_cast<const double2*>(R8 + 4 * t + 2);
+    return fma(d.y, x1, d.x * x0);
+  };
+  auto c8 = [&]() { return *reinterpret_cast<const double2*>(R8 + 16 + 2 * g); };  // (B8[g], D8[g])
+  auto f8B = [&]() { return *reinterpret_cast<const double2*>(rB + 2 * t); };     // (B8[2t], B8[2t+1])
+  auto f8D = [&]() { return *reinterpret_cast<const double2*>(rD + 2 * t); };
 
   const double* Gcol = A.G + static_cast<long long>(col) * nz * GSE;
   constexpr uint32_t gbytes = GSE * 8;
@@ -193,8 +219,8 @@ __global__ void __launch_bounds__(NT, 2)
     dmma(cb0, cb1, aB1, b[1]);
     dmma(cd0, cd1, aD0, b[0]);
     dmma(cd0, cd1, aD1, b[1]);
-    const double r8b = quad_sum(fma(rB[t + 4], b[1], rB[t] * b[0]));
-    const double r8d = quad_sum(fma(rD[t + 4], b[1], rD[t] * b[0]));
+    const double r8b = quad_sum(row8B(b[0], b[1]));
+    const double r8d = quad_sum(row8D(b[0], b[1]));
     // SA[f][j = G][8 a3 + i]: rows a3 = g, cols i = 2t, 2t+1; row a3 = 8 at i = g
     double* sa = SA + G * SA_KS;
     const int h = swa(G);
@@ -218,9 +244,9 @@ __global__ void __launch_bounds__(NT, 2)
     dmma(db0, db1, aD1, x01);
     dmma(bd0, bd1, aB0, x10);
     dmma(bd0, bd1, aB1, x11);
-    const double r8bb = quad_sum(fma(rB[t + 4], x01, rB[t] * x00));
-    const double r8db = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));
-    const double r8bd = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
+    const double r8bb = quad_sum(row8B(x00, x01));
+    const double r8db = quad_sum(row8D(x00, x01));
+    const double r8bd = quad_sum(row8B(x10, x11));
     // SB[f][k = i][p = b + 9c]; rows b = g, cols i = 2t, 2t+1
     const int i0 = sbi(2 * t, g + 9 * G), i1 = sbi(2 * t + 1, g + 9 * G);
     SB[i0] = bb0;
@@ -255,9 +281,9 @@ __global__ void __launch_bounds__(NT, 2)
     dmma(gs[0], gs[1], x11, aB1);
     dmma(gt[0], gt[1], x20, aB0);
     dmma(gt[0], gt[1], x21, aB1);
-    double r8r = quad_sum(fma(rD[t + 4], x01, rD[t] * x00));  // a = 8 of pencil g (all 4 lanes)
-    double r8s = quad_sum(fma(rB[t + 4], x11, rB[t] * x10));
-    double r8t = quad_sum(fma(rB[t + 4], x21, rB[t] * x20));
+    double r8r = quad_sum(row8D(x00, x01));  // a = 8 of pencil g (all 4 lanes)
+    double r8s = quad_sum(row8B(x10, x11));
+    double r8t = quad_sum(row8B(x20, x21));
     const int p = 8 * G + g;
     if (p < QQ) {
       // pointwise factors (operator.hpp:129-131); [qp][6] layout, qp = a + 9p:
@@ -280,12 +306,13 @@ __global__ void __launch_bounds__(NT, 2)
     }
     // backward: W[p][i] = sum_a A[p][a] M[a][i]; a = 8 term first
     double w1[2], w2[2], w3[2];
-    w1[0] = rD[2 * t] * r8r;
-    w1[1] = rD[2 * t + 1] * r8r;
-    w2[0] = rB[2 * t] * r8s;
-    w2[1] = rB[2 * t + 1] * r8s;
-    w3[0] = rB[2 * t] * r8t;
-    w3[1] = rB[2 * t + 1] * r8t;
+    const double2 fd = f8D(), fb = f8B();
+    w1[0] = fd.x * r8r;
+    w1[1] = fd.y * r8r;
+    w2[0] = fb.x * r8s;
+    w2[1] = fb.y * r8s;
+    w3[0] = fb.x * r8t;
+    w3[1] = fb.y * r8t;
     dmma(w1[0], w1[1], gr[0], eD0);
     dmma(w1[0], w1[1], gr[1], eD1);
     dmma(w2[0], w2[1], gs[0], eB0);
@@ -313,10 +340,11 @@ __global__ void __launch_bounds__(NT, 2)
     const double2 e2 = *reinterpret_cast<const double2*>(s8 + SA_F);
     const double2 e3 = *reinterpret_cast<const double2*>(s8 + 2 * SA_F);
     double c1[2], c2[2];
-    c1[0] = fma(rD[g], e2.x, rB[g] * e1.x);
-    c1[1] = fma(rD[g], e2.y, rB[g] * e1.y);
-    c2[0] = rB[g] * e3.x;
-    c2[1] = rB[g] * e3.y;
+    const double2 bd8 = c8();
+    c1[0] = fma(bd8.y, e2.x, bd8.x * e1.x);
+    c1[1] = fma(bd8.y, e2.y, bd8.x * e1.y);
+    c2[0] = bd8.x * e3.x;
+    c2[1] = bd8.x * e3.y;
     dmma(c1[0], c1[1], tB0, y00);
     dmma(c1[0], c1[1], tB1, y01);
     dmma(c1[0], c1[1], tD0, y10);
@@ -342,8 +370,9 @@ __global__ void __launch_bounds__(NT, 2)
     const double2 e1 = *reinterpret_cast<const double2*>(s8);
     const double2 e2 = *reinterpret_cast<const double2*>(s8 + SC_F);
     double o[2];
-    o[0] = fma(rD[g], e2.x, rB[g] * e1.x);
-    o[1] = fma(rD[g], e2.y, rB[g] * e1.y);
+    const double2 bd8 = c8();
+    o[0] = fma(bd8.y, e2.x, bd8.x * e1.x);
+    o[1] = fma(bd8.y, e2.y, bd8.x * e1.y);
     dmma(o[0], o[1], tB0, z00);
     dmma(o[0], o[1], tB1, z01);
     dmma(o[0], o[1], tD0, z10);

@@ -81,29 +81,54 @@ def algorithmic_bytes(bp: int, p: int, dims):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks / throttle reasons sampled during the timed region: NVML every
+    10 ms (a timed region of 20 CG iterations lasts ~0.1 s), nvidia-smi if NVML
+    is unavailable."""
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, sm_max_mhz, [reasons])
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _sample_nvml(self):
+        import pynvml as N
+
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": N.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": N.nvmlClocksThrottleReasonSwPowerCap}
         while not self._stop.is_set():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.rows.append((float(sm), float(mx), [k for k, b in bits.items() if r & b]))
+            self._stop.wait(0.01)
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            f = [x.strip() for x in out.split(",")]
+            if len(f) >= 6 and f[0].replace(".", "").isdigit():
+                self.rows.append((float(f[0]), float(f[1]),
+                                  [names[i] for i in range(4) if "Active" in f[2 + i] and "Not" not in f[2 + i]]))
+            self._stop.wait(0.05)
+
+    def _run(self):
+        try:
+            self._sample_nvml()
+        except Exception:
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -117,13 +142,8 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
-                          and "Not" not in r[5 + i]})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({x for r in self.rows for x in r[2]}), "samples": len(self.rows)}
 
 
 def cpu_baseline(bp: int, p: int, steps: int = 3):
@@ -246,17 +266,27 @@ def main():
     t_ref = ev0.elapsed_time(ev1) / 1e3
     op.workspace().set_mode("fast")
 
-    # operator kernel alone: CUDA events around R back-to-back applies on the launch stream
+    # the dominant kernel alone: CUDA events around R back-to-back launches of
+    # the operator kernel on the launch stream, in the form the CG runs it
+    # (ring nodes left as column partials for the r-update: hexbp_apply_ring_deferred)
     u = torch.empty_like(b).uniform_(-1, 1)
     w = torch.empty_like(b)
+    con = 1 if bp != 1 else 0
+    sp = C.c_void_p(st.cuda_stream)
+
+    def kernel_once():
+        rc = L.hexbp_apply_ring_deferred(setup._h, op.workspace()._h, C.c_void_p(u.data_ptr()),
+                                         C.c_void_p(w.data_ptr()), con, sp)
+        assert rc == 0, L.hexbp_last_error()
+
     for _ in range(3):
-        A.apply(u, w)
+        kernel_once()
     R = 10
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ea.record(st)
     for _ in range(R):
-        A.apply(u, w)
+        kernel_once()
     eb.record(st)
     torch.cuda.synchronize()
     t_apply = ea.elapsed_time(eb) / 1e3 / R
@@ -302,15 +332,17 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "kernel": ("bp3_p7_mma_kernel (DMMA)" if (bp == 3 and p == 7) else "bp_apply_kernel") +
-                               " + lateral_fixup_kernel, timed together per apply",
+                               " (ring nodes as column partials, summed by the CG r-update)",
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "algorithmic_bytes_per_launch": b_op, "apply_ms": t_apply * 1e3},
+                     "algorithmic_bytes_per_launch": b_op, "kernel_ms": t_apply * 1e3},
         "cg_iteration_roofline": {"algorithmic_bytes_per_iter": b_it, "achieved_GBps": b_it * K / t_dev / 1e9,
                                   "frac": b_it * K / t_dev / 1e9 / peak,
                                   "roofline_GDOFps": peak * 1e9 / (b_it / nL) / 1e9},
         "e2e": {"value": e2e, "unit": "GDOF/s", "h2d_bytes_per_step": 2 * n * 8 / K, "d2h_bytes_per_step": n * 8 / K,
                 "path": "hexbp_cg_host (C ABI, pinned host b/x; b, x0 in and x out per solve, amortised per step)"},
-        "gpu_launches": 4 * K + 3,
+        # per CG iteration: operator, ring-summing r-update, x/p update; plus the
+        # initial residual (operator, ring fix-up, init)
+        "gpu_launches": 3 * K + 3,
         "reference_mode": {"GDOFps": n * K / t_ref / 1e9, "ms_per_step": t_ref / K * 1e3,
                            "note": "bit-exact reference arithmetic (same iterates as the CPU reference)",
                            "final_rel_residual": rep_ref.final_rel_residual},

@@ -116,6 +116,16 @@ int hexbp_workspace_set_mode(hexbp_workspace_t ws, int mode);
 int hexbp_apply(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, double* w_dev, int constrained,
                 void* stream);
 
+/* The fast-mode operator kernel alone (HEXBP_MODE_FAST workspaces only): as
+ * hexbp_apply, except that the nodes shared between element columns (the
+ * "ring" of each column footprint, 4p per node plane) are left as column
+ * partial sums in the workspace instead of being summed into w -- the form
+ * the fast CG consumes (its r-update adds them, restriction.hpp:67-80 order).
+ * w is final on every other node. For fused callers and for timing the
+ * dominant kernel. */
+int hexbp_apply_ring_deferred(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, double* w_dev,
+                              int constrained, void* stream);
+
 /* Same, with HOST buffers of n doubles; synchronous (drop-in for the
  * reference's std::span / std::vector signature). */
 int hexbp_apply_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* u, double* w, int64_t n, int constrained);

@@ -92,7 +92,7 @@ constexpr int best_stride(int N, int Q, int base, int kind) {
 }
 
 template <int P, int Q>
-struct BasisT {
+struct alignas(16) BasisT {  // 16-byte aligned kernel parameter: paired constant loads (LDCU.128)
   double B[Q][P + 1];
   double D[Q][P + 1];
 };
@@ -116,7 +116,11 @@ struct Cfg {
   static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
   // ptxas sizes the register cap as if CTAs were whole 4-warp groups; these
   // values leave the cap at 255 and let registers/smem set the occupancy.
-  static constexpr int MIN_BLOCKS = NT <= 32 ? 8 : (NT <= 64 ? 4 : (NT <= 96 ? 3 : 2));
+  // (P = 4 stiffness: ptxas spills uniform registers into vector registers
+  // (R2UR per basis coefficient) and reaches 194 registers unless capped; six
+  // CTAs per SM measured faster despite a small spill.)
+  static constexpr int MIN_BLOCKS =
+      NT <= 32 ? 8 : (NT <= 64 ? (P == 4 && KIND != KIND_MASS ? 6 : 4) : (NT <= 96 ? 3 : 2));
 };
 
 template <int P, int Q, int KIND>
@@ -421,27 +425,42 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
       // ---------------- transpose restriction, part 1 (see header)
       out[0] += carry;
       const int kend = (ez == A.nz - 1) ? N : P;
+      const double* usz = Us + (ez & 1) * N * N * N + t;  // u of this element, still staged
+      if (!do_dot) {  // plain apply: the lean epilogue (keeps ptxas' uniform registers for the basis)
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (k < kend) {
-          const int Z = ez * P + k;
-          if (ring) {
-            lat[Z * lat_stride] = out[k];
-            if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
+        for (int k = 0; k < N; ++k) {
+          if (k < kend) {
+            const int Z = ez * P + k;
+            if (ring) {
+              lat[Z * lat_stride] = out[k];
+            } else {
               const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-              const double uv = __ldg(A.u + node);
-              if (bcxy || (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)))) {
-                if (owner) dot = fma(uv, uv, dot);  // w = u, counted once
-              } else {
-                dot = fma(uv, out[k], dot);
-              }
+              double v = out[k];
+              if (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = usz[k * N * N];
+              A.w[node] = v;
             }
-          } else {
-            const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-            double v = out[k];
-            if (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = __ldg(A.u + node);
-            A.w[node] = v;
-            if (do_dot) dot = fma(__ldg(A.u + node), v, dot);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          if (k < kend) {
+            const int Z = ez * P + k;
+            const double uv = usz[k * N * N];
+            const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+            if (ring) {
+              lat[Z * lat_stride] = out[k];
+              // column-local share of p.Ap on the ring (ring.cuh); w = u rows counted once
+              if (bcxy || zbc)
+                dot = owner ? fma(uv, uv, dot) : dot;
+              else
+                dot = fma(uv, out[k], dot);
+            } else {
+              const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+              const double v = zbc ? uv : out[k];
+              A.w[node] = v;
+              dot = fma(uv, v, dot);
+            }
           }
         }
       }

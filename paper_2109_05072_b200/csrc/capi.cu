@@ -382,6 +382,17 @@ int hexbp_apply(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* 
   return HEXBP_OK;
 }
 
+int hexbp_apply_ring_deferred(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* w, int constrained,
+                              void* stream) {
+  if (!h || !wh || !u || !w) return invalid("apply: null argument");
+  if (wh->w.s != &h->s) return invalid("apply: workspace belongs to another setup");
+  if (u == w) return invalid("apply: u and w must not alias");
+  if (wh->w.exact) return invalid("apply_ring_deferred: fast-mode workspaces only");
+  DeviceGuard g(h->s.device);
+  CK(launch_apply(h->s, wh->w, u, w, constrained, nullptr, nullptr, static_cast<cudaStream_t>(stream), false));
+  return HEXBP_OK;
+}
+
 int hexbp_apply_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* w, int64_t n, int constrained) {
   if (!h || !wh || !u || !w) return invalid("apply: null argument");
   if (n != h->s.nL) return invalid("apply: L-vector length mismatch");  // operator.hpp:268

@@ -51,13 +51,13 @@ struct ApplyArgs {
   int constrained;          // ConstrainedOperator semantics (solver.hpp:60-65)
   int bc_zlo, bc_zhi;       // z-faces that are essential (slab partitions)
   double* lateral;          // ring partials: exact mode [Z][column][4p]; fast mode latY (ring.cuh)
-  double* lat_x;            // fast mode: latX (ring.cuh)
   double* zupper;           // exact mode: upper-layer ring partials of z-shared planes [ez][column][4p]
   double* col_dot;          // per-column partial p.Ap (nullptr: no dot)
   double* fix_partials;     // per-block partial p.Ap of the lateral fix-up
   unsigned int* fix_done;
   DevScalars* sc;           // CG scalars (nullptr: plain apply)
   double* dot_out;          // where the final dot lands (nullptr: CG alpha logic only)
+  double* lat_x;            // fast mode: latX (ring.cuh)
 };
 
 struct Setup {

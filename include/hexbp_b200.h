@@ -139,6 +139,24 @@ int hexbp_apply_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* u, dou
 int hexbp_cg(hexbp_setup_t s, hexbp_workspace_t ws, const double* b_dev, double* x_dev, double rel_tol, int max_iter,
              int constrained, hexbp_cg_report* report, double* history, void* stream);
 
+/* cg with the Jacobi preconditioner z = r / diag (solver.hpp:91-153 with
+ * `diag`, :105-108): diag_dev holds l_size doubles on the device, NULL gives
+ * hexbp_cg. Same reports, modes and error semantics as hexbp_cg; reference
+ * mode reproduces the reference's preconditioned iterates bit for bit. */
+int hexbp_pcg(hexbp_setup_t s, hexbp_workspace_t ws, const double* b_dev, double* x_dev, const double* diag_dev,
+              double rel_tol, int max_iter, int constrained, hexbp_cg_report* report, double* history, void* stream);
+
+/* jacobi_diagonal (solver.hpp:155-205) computed on the device in the
+ * reference's arithmetic (bit for bit): the operator's diagonal, or with
+ * constrained = 1 the ConstrainedOperator's (1 on the essential dofs).
+ * diag_dev: l_size doubles. Setup-time call: allocates a temporary element
+ * vector; synchronous. */
+int hexbp_jacobi_diagonal(hexbp_setup_t s, int constrained, double* diag_dev, void* stream);
+
+/* Same as hexbp_pcg with HOST b, x and diag (diag may be NULL). */
+int hexbp_pcg_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* b, double* x, const double* diag, int64_t n,
+                   double rel_tol, int max_iter, int constrained, hexbp_cg_report* report, double* history);
+
 /* Same with HOST b and x (x0 in, solution out). */
 int hexbp_cg_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* b, double* x, int64_t n, double rel_tol,
                   int max_iter, int constrained, hexbp_cg_report* report, double* history);

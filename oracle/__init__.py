@@ -145,19 +145,36 @@ class Oracle:
             raise RuntimeError(self._fn("last_error")().decode())
         return w
 
+    def jacobi_diagonal(self, constrained: bool = True) -> np.ndarray:
+        """jacobi_diagonal (solver.hpp:155-205)."""
+        out = np.zeros(self.n)
+        f = self._fn("jacobi_diagonal")
+        f.argtypes = [C.c_void_p, C.c_int, _dp]
+        f(self.h, int(constrained), _ptr(out))
+        return out
+
     def bench_rhs(self, seed: int = 20240101) -> np.ndarray:
         b = np.zeros(self.n)
         self._fn("bench_rhs")(self.h, C.c_uint64(seed), _ptr(b))
         return b
 
-    def cg(self, b, x0=None, rel_tol: float = 1e-8, max_iter: int = 2000, constrained: bool = True):
+    def cg(self, b, x0=None, rel_tol: float = 1e-8, max_iter: int = 2000, constrained: bool = True, diag=None):
         b = _f64(b)
         x = np.zeros(self.n) if x0 is None else _f64(x0).copy()
         it, conv, fr = C.c_int(0), C.c_int(0), C.c_double(0.0)
         hist = np.zeros(max_iter + 1)
         extra = self._cg_extra_args()
-        rc = self._fn("cg")(self.h, int(constrained), _ptr(b), _ptr(x), rel_tol, max_iter, C.byref(it),
-                            C.byref(conv), C.byref(fr), _ptr(hist), *extra)
+        if diag is None:
+            rc = self._fn("cg")(self.h, int(constrained), _ptr(b), _ptr(x), rel_tol, max_iter, C.byref(it),
+                                C.byref(conv), C.byref(fr), _ptr(hist), *extra)
+        else:  # Jacobi-preconditioned (solver.hpp:105-108)
+            d = _f64(diag)
+            assert d.size == self.n
+            f = self._fn("pcg")
+            f.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_double, C.c_int, C.POINTER(C.c_int),
+                          C.POINTER(C.c_int), C.POINTER(C.c_double), _dp] + self._cg_extra()
+            rc = f(self.h, int(constrained), _ptr(b), _ptr(x), _ptr(d), rel_tol, max_iter, C.byref(it),
+                   C.byref(conv), C.byref(fr), _ptr(hist), *extra)
         if rc == 2:
             raise ArithmeticError("divergence_error: " + self._fn("last_error")().decode())
         if rc:

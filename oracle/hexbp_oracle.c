@@ -721,6 +721,120 @@ done:
   return status;
 }
 
+/* jacobi_diagonal, solver.hpp:155-205: element diagonals (loops k, j, i over
+ * nodes, c, b, a over quadrature points, the reference's expression order)
+ * scattered with scatter_add's ascending-slot order; constrained: 1 on the
+ * essential dofs (solver.hpp:200-205). */
+void or_jacobi_diagonal(void* hv, int constrained, double* out) {
+  Problem* h = hv;
+  const Basis* bs = &h->basis;
+  const int n = bs->n, q = bs->q, nen = h->nen;
+  const int diff = h->bp != 1;
+  double* de = malloc(sizeof(double) * nen);
+  memset(out, 0, sizeof(double) * h->nL);
+#define BB(a, i) bs->B[(a) * n + (i)]
+#define DD(a, i) bs->D[(a) * n + (i)]
+  for (int e = 0; e < h->E; ++e) {
+    const double* f = h->factors + (size_t)e * h->q3 * h->comp;
+    for (int k = 0; k < n; ++k)
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) {
+          double sum = 0.0;
+          for (int c = 0; c < q; ++c)
+            for (int b = 0; b < q; ++b)
+              for (int a = 0; a < q; ++a) {
+                const int qp = a + q * (b + q * c);
+                if (diff) {
+                  const double* g = f + (size_t)qp * 6;
+                  const double dr = DD(a, i) * BB(b, j) * BB(c, k);
+                  const double ds = BB(a, i) * DD(b, j) * BB(c, k);
+                  const double dt = BB(a, i) * BB(b, j) * DD(c, k);
+                  sum += g[0] * dr * dr + g[3] * ds * ds + g[5] * dt * dt +
+                         2.0 * (g[1] * dr * ds + g[2] * dr * dt + g[4] * ds * dt);
+                } else {
+                  const double phi = BB(a, i) * BB(b, j) * BB(c, k);
+                  sum += f[qp] * phi * phi;
+                }
+              }
+          de[i + n * (j + n * k)] = sum;
+        }
+    /* scatter_add (restriction.hpp:67-80): ascending slots = ascending e */
+    const int* nodes = h->elem_nodes + (size_t)e * nen;
+    for (int l = 0; l < nen; ++l) out[nodes[l]] += de[l];
+  }
+#undef BB
+#undef DD
+  free(de);
+  if (constrained)
+    for (int64_t i = 0; i < h->nb; ++i) out[h->bdofs[i]] = 1.0;
+}
+
+/* cg with the optional Jacobi preconditioner z = r / diag (solver.hpp:91-153);
+ * diag == NULL is or_cg. */
+int or_pcg(void* hv, int constrained, const double* b, double* x, const double* diag, double rel_tol, int max_iter,
+           int* iterations, int* converged, double* final_rel, double* history) {
+  Problem* h = hv;
+  const int64_t n = h->nL;
+  double* r = malloc(sizeof(double) * n);
+  double* z = malloc(sizeof(double) * n);
+  double* p = malloc(sizeof(double) * n);
+  double* Ap = malloc(sizeof(double) * n);
+  int status = 0;
+  *iterations = 0;
+  *converged = 0;
+  or_apply(h, constrained, x, Ap);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - Ap[i];
+  const double r0 = sqrt(or_dot(r, r, n));
+  int hl = 0;
+  history[hl++] = r0;
+  if (!isfinite(r0)) {
+    status = 2;
+    goto done;
+  }
+  if (r0 == 0.0) {
+    *converged = 1;
+    *final_rel = 0.0;
+    goto done;
+  }
+  for (int64_t i = 0; i < n; ++i) z[i] = diag ? r[i] / diag[i] : r[i];
+  memcpy(p, z, sizeof(double) * n);
+  double rz = or_dot(r, z, n);
+  for (int k = 1; k <= max_iter; ++k) {
+    or_apply(h, constrained, p, Ap);
+    const double pAp = or_dot(p, Ap, n);
+    if (!isfinite(pAp) || pAp <= 0.0) {
+      status = 2;
+      goto done;
+    }
+    const double alpha = rz / pAp;
+    for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+    for (int64_t i = 0; i < n; ++i) r[i] -= alpha * Ap[i];
+    const double rnorm = sqrt(or_dot(r, r, n));
+    if (!isfinite(rnorm)) {
+      status = 2;
+      goto done;
+    }
+    history[hl++] = rnorm;
+    *iterations = k;
+    if (rnorm / r0 <= rel_tol) {
+      *converged = 1;
+      break;
+    }
+    for (int64_t i = 0; i < n; ++i) z[i] = diag ? r[i] / diag[i] : r[i];
+    const double rz_next = or_dot(r, z, n);
+    const double beta = rz_next / rz;
+    rz = rz_next;
+    for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  }
+  *final_rel = history[hl - 1] / r0;
+done:
+  free(r);
+  free(z);
+  free(p);
+  free(Ap);
+  return status;
+}
+
 /* ------------------------------------------------------------------ */
 /* seeded inputs: std::mt19937_64 + uniform_real_distribution(-1,1)    */
 /* (libstdc++ generate_canonical with one 64-bit draw)                 */

@@ -43,6 +43,12 @@ int or_apply(void* h, int constrained, const double* u, double* w);
 int or_cg(void* h, int constrained, const double* b, double* x, double rel_tol, int max_iter, int* iterations,
           int* converged, double* final_rel, double* history);
 
+/* jacobi_diagonal (solver.hpp:155-205); constrained: 1 on essential dofs */
+void or_jacobi_diagonal(void* h, int constrained, double* out);
+/* cg with Jacobi preconditioner z = r / diag (diag may be NULL) */
+int or_pcg(void* h, int constrained, const double* b, double* x, const double* diag, double rel_tol, int max_iter,
+           int* iterations, int* converged, double* final_rel, double* history);
+
 double or_dot(const double* a, const double* b, int64_t n);
 void or_bench_rhs(void* h, uint64_t seed, double* b);
 void or_random_vector(uint64_t seed, int64_t n, double* out);

@@ -7,7 +7,7 @@
 // reference's own code:
 //   - make_setup + OperatorHandle(Fused)      (operator.hpp:70-77, 244-279)
 //   - ConstrainedOperator                     (solver.hpp:48-74)
-//   - cg                                      (solver.hpp:91-153)
+//   - cg, jacobi_diagonal                     (solver.hpp:91-205)
 //   - run_bench (reference timing protocol)   (bench.hpp:214-295)
 //   - check_equivalence (72-case sweep)       (verify.hpp:50-108)
 // No reference source is copied here; the headers are #included from their
@@ -150,6 +150,45 @@ int ref_cg(void* hv, int constrained, const double* b, double* x, double rel_tol
         h->op->apply(u, w);
     };
     CGReport r = cg(apply, std::span<const double>(b, n), xv, rel_tol, max_iter);
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+    *iterations = r.iterations;
+    *converged = r.converged ? 1 : 0;
+    *final_rel = r.final_rel_residual;
+    *seconds = r.seconds;
+    for (std::size_t k = 0; k < r.residual_history.size(); ++k) history[k] = r.residual_history[k];
+    return 0;
+  } catch (const divergence_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// jacobi_diagonal (solver.hpp:155-205) of the operator (constrained = 0) or
+// of the ConstrainedOperator (1 on essential dofs).
+void ref_jacobi_diagonal(void* hv, int constrained, double* out) {
+  auto* h = static_cast<RefHandle*>(hv);
+  const std::vector<double> d = constrained ? jacobi_diagonal(*h->cop) : jacobi_diagonal(*h->op);
+  std::memcpy(out, d.data(), sizeof(double) * d.size());
+}
+
+// cg with the Jacobi diagonal (solver.hpp:91-153, diag != nullptr).
+int ref_pcg(void* hv, int constrained, const double* b, double* x, const double* diag, double rel_tol, int max_iter,
+            int* iterations, int* converged, double* final_rel, double* history, double* seconds) {
+  auto* h = static_cast<RefHandle*>(hv);
+  try {
+    const std::size_t n = h->op->size();
+    std::vector<double> xv(x, x + n);
+    const std::vector<double> dv(diag, diag + n);
+    auto apply = [&](std::span<const double> u, std::vector<double>& w) {
+      if (constrained)
+        h->cop->apply(u, w);
+      else
+        h->op->apply(u, w);
+    };
+    CGReport r = cg(apply, std::span<const double>(b, n), xv, rel_tol, max_iter, &dv);
     std::memcpy(x, xv.data(), sizeof(double) * n);
     *iterations = r.iterations;
     *converged = r.converged ? 1 : 0;

@@ -31,6 +31,7 @@ from .api import (  # noqa: F401
     device_count,
     divergence_error,
     is_diffusion,
+    jacobi_diagonal,
     make_operator,
     make_setup,
     make_slab_setup,

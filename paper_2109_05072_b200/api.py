@@ -454,8 +454,6 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
     x0 on entry and the solution on exit (numpy arrays are updated in place).
     ``reduction='reference'`` reproduces deterministic_dot and the reference's
     vector arithmetic bit for bit; ``'fused'`` fuses p.Ap into the operator."""
-    if diag is not None:
-        raise NotImplementedError("Jacobi-preconditioned CG is a SURVEY §8(f) next row")
     if isinstance(apply_op, ConstrainedOperator):
         op, constrained = apply_op.raw(), 1
     elif isinstance(apply_op, OperatorHandle):
@@ -472,19 +470,56 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
         _check_device_vec(b, n, "cg")
         if not _is_torch(x) or x.numel() != n:
             raise ValueError("cg: x0 length mismatch")
-        rc = _lib.lib().hexbp_cg(op.setup()._h, ws._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), rel_tol,
-                                 max_iter, constrained, C.byref(rep), hist.ctypes.data_as(_dp), _stream_ptr(b))
+        dptr = None
+        if diag is not None:  # Jacobi preconditioner (solver.hpp:105-108)
+            import torch
+
+            if not _is_torch(diag):
+                diag = torch.as_tensor(np.ascontiguousarray(diag, np.float64), device=b.device)
+            if diag.numel() != n:
+                raise ValueError("cg: diagonal length mismatch")  # solver.hpp:97
+            _check_device_vec(diag, n, "cg")
+            dptr = C.c_void_p(diag.data_ptr())
+        rc = _lib.lib().hexbp_pcg(op.setup()._h, ws._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), dptr,
+                                  rel_tol, max_iter, constrained, C.byref(rep), hist.ctypes.data_as(_dp),
+                                  _stream_ptr(b))
     else:
         b = np.ascontiguousarray(b, np.float64)
         if not isinstance(x, np.ndarray) or x.dtype != np.float64 or x.size != n or not x.flags.c_contiguous:
             raise ValueError("cg: x0 length mismatch")
         if b.size != n:
             raise ValueError("cg: b length mismatch")
-        rc = _lib.lib().hexbp_cg_host(op.setup()._h, ws._h, b.ctypes.data_as(_dp), x.ctypes.data_as(_dp), n, rel_tol,
-                                      max_iter, constrained, C.byref(rep), hist.ctypes.data_as(_dp))
+        dh = None
+        if diag is not None:
+            d = diag.detach().cpu().numpy() if _is_torch(diag) else diag
+            dh = np.ascontiguousarray(d, np.float64)
+            if dh.size != n:
+                raise ValueError("cg: diagonal length mismatch")  # solver.hpp:97
+        rc = _lib.lib().hexbp_pcg_host(op.setup()._h, ws._h, b.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
+                                       dh.ctypes.data_as(_dp) if dh is not None else None, n, rel_tol, max_iter,
+                                       constrained, C.byref(rep), hist.ctypes.data_as(_dp))
     _check(rc)
     return CGReport(rep.iterations, bool(rep.converged), rep.final_rel_residual, hist[: rep.iterations + 1].copy(),
                     time.perf_counter() - t0)
+
+
+def jacobi_diagonal(op, device: bool = True):
+    """jacobi_diagonal (solver.hpp:155-205) of an OperatorHandle, or of a
+    ConstrainedOperator (1 on the essential dofs), computed on the GPU in the
+    reference's arithmetic (bit for bit). Returns a device tensor, or a numpy
+    array with device=False."""
+    import torch
+
+    if isinstance(op, ConstrainedOperator):
+        raw, constrained = op.raw(), 1
+    elif isinstance(op, OperatorHandle):
+        raw, constrained = op, 0
+    else:
+        raise TypeError("jacobi_diagonal: expected an OperatorHandle or ConstrainedOperator")
+    setup = raw.setup()
+    d = torch.empty(raw.size(), dtype=torch.float64, device=torch.device("cuda", setup.device))
+    _check(_lib.lib().hexbp_jacobi_diagonal(setup._h, constrained, C.c_void_p(d.data_ptr()), _stream_ptr(d)))
+    return d if device else d.cpu().numpy()
 
 
 def bench_rhs(kind, p: int, dims, seed: int = 20240101, offset: int = 0, count: Optional[int] = None) -> np.ndarray:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstddef>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -408,6 +409,41 @@ int hexbp_apply_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, dou
 
 int hexbp_cg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, double rel_tol, int max_iter,
              int constrained, hexbp_cg_report* report, double* history, void* stream) {
+  return hexbp_pcg(h, wh, b, x, nullptr, rel_tol, max_iter, constrained, report, history, stream);
+}
+
+int hexbp_jacobi_diagonal(hexbp_setup_t h, int constrained, double* diag, void* stream) {
+  if (!h || !diag) return invalid("jacobi_diagonal: null argument");
+  DeviceGuard g(h->s.device);
+  const cudaError_t e = launch_jacobi_diagonal(h->s, constrained, diag, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorMemoryAllocation) return cuda_status(e, "jacobi_diagonal: element vector");
+  CK(e);
+  return HEXBP_OK;
+}
+
+int hexbp_pcg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, int64_t n,
+                   double rel_tol, int max_iter, int constrained, hexbp_cg_report* report, double* history) {
+  if (!h || !wh || !b || !x) return invalid("cg: null argument");
+  if (n != h->s.nL) return invalid("cg: x0 length mismatch");  // solver.hpp:96
+  DeviceGuard g(h->s.device);
+  Workspace& w = wh->w;
+  int rc = ensure_host_staging(w);
+  if (rc) return rc;
+  double* dd = nullptr;
+  if (diag) {
+    CK(cudaMalloc(&dd, sizeof(double) * n));
+    CK(cudaMemcpy(dd, diag, sizeof(double) * n, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(w.tmp_u, b, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(w.tmp_w, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  rc = hexbp_pcg(h, wh, w.tmp_u, w.tmp_w, dd, rel_tol, max_iter, constrained, report, history, nullptr);
+  if (dd) cudaFree(dd);
+  if (rc == HEXBP_OK || rc == HEXBP_DIVERGENCE) CK(cudaMemcpy(x, w.tmp_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return rc;
+}
+
+int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, double rel_tol,
+              int max_iter, int constrained, hexbp_cg_report* report, double* history, void* stream) {
   if (!h || !wh || !b || !x) return invalid("cg: null argument");
   if (max_iter < 0) return invalid("cg: max_iter must be >= 0");
   const auto t0 = std::chrono::steady_clock::now();
@@ -422,9 +458,26 @@ int hexbp_cg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, 
     CK(cudaMalloc(&w.history, sizeof(double) * w.history_cap));
   }
   const int64_t n = s.nL;
+  // Jacobi preconditioner for this solve (DevScalars::precond selects the
+  // r.z recurrence of beta in the kernels' scalar logic)
+  w.diag = diag;
+  {
+    const int pc = diag ? 1 : 0;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(w.sc) + offsetof(DevScalars, precond), &pc, sizeof(int),
+                       cudaMemcpyHostToDevice, st));
+  }
+  struct ClearDiag {  // the workspace's other solvers (multi-GPU CG) run unpreconditioned
+    Workspace& w;
+    cudaStream_t st;
+    ~ClearDiag() {
+      w.diag = nullptr;
+      cudaMemsetAsync(reinterpret_cast<char*>(w.sc) + offsetof(DevScalars, precond), 0, sizeof(int), st);
+    }
+  } clear_diag{w, st};
   // r0 = b - A x0 (solver.hpp:102-103)
   CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
   CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
+  if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz = r0.z0 (solver.hpp:124)
   const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
   for (int k = 1; k <= max_iter; ++k) {
     if (w.exact) {
@@ -434,6 +487,7 @@ int hexbp_cg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, 
       CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
     }
     CK(launch_cg_update_r(w, n, st, constrained));
+    if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz_next = r.z, beta (solver.hpp:145-147)
     CK(launch_cg_update_xp(w, x, n, st));
     if (k % check_every == 0 && k < max_iter) {
       CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));

@@ -41,6 +41,7 @@ constexpr int TSTRIDE = TILE + 1;    // smem row stride (conflict-free column wa
 #define DM(a, b) __dmul_rn((a), (b))
 #define DA(a, b) __dadd_rn((a), (b))
 #define DS(a, b) __dsub_rn((a), (b))
+#define DD(a, b) __ddiv_rn((a), (b))
 
 __device__ __forceinline__ bool last_block(unsigned int* done) {
   __shared__ int s_last;
@@ -69,13 +70,15 @@ __device__ __forceinline__ double serial_sum(const double* part, long long n) {
   return s;
 }
 
-enum Op : int { OP_DOT = 0, OP_PAP = 1, OP_INIT = 2, OP_UPDATE_R = 3 };
+enum Op : int { OP_DOT = 0, OP_PAP = 1, OP_INIT = 2, OP_UPDATE_R = 3, OP_RZ = 4 };
 
 // Blocked exact reduction with an optional fused elementwise update.
 //   OP_DOT      : dot(a, b)                                   -> *out
 //   OP_PAP      : dot(p=a, Ap=b); alpha = rz / pAp            (solver.hpp:128-131)
 //   OP_INIT     : r = b - Ap (a=b_rhs, b=Ap, w0=r, w1=p); p = r; r.r; r0  (solver.hpp:102-124)
 //   OP_UPDATE_R : r = r - alpha Ap (a=r, b=Ap, w0=r); r.r; rnorm, stop, beta (solver.hpp:133-147)
+//   OP_RZ       : r.z with z = r / diag (a=r, b=diag) -> rz (init) or beta, rz (solver.hpp:108,145-147)
+// With a Jacobi diagonal `dv`, OP_INIT stores p = z = r / diag.
 __device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, double rel_tol, int max_iter);
 
 // `owned` >= 0: elementwise updates run over [0, n) but only entries
@@ -86,11 +89,11 @@ __global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, con
                                                             double* w1, long long n, double* part,
                                                             unsigned int* done, DevScalars* sc, double* hist,
                                                             double* out, double rel_tol, int max_iter,
-                                                            long long owned = -1) {
+                                                            long long owned = -1, const double* dv = nullptr) {
   __shared__ double prod[CPB * TSTRIDE];
   const bool dist = owned >= 0;
   const long long lo = dist ? owned : 0;
-  if (OP == OP_PAP || OP == OP_UPDATE_R) {
+  if (OP == OP_PAP || OP == OP_UPDATE_R || OP == OP_RZ) {
     if (*(volatile int*)&sc->status != ST_RUNNING) return;
   }
   const double alpha = OP == OP_UPDATE_R ? sc->alpha : 0.0;
@@ -108,10 +111,12 @@ __global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, con
         const double x = a[g], y = b[g];
         if (OP == OP_DOT || OP == OP_PAP) {
           pr = DM(x, y);
+        } else if (OP == OP_RZ) {
+          pr = DM(x, DD(x, y));  // r * (r / diag)
         } else if (OP == OP_INIT) {
           const double r = DS(x, y);  // r = b - Ap (solver.hpp:103)
           w0[g] = r;
-          w1[g] = r;  // z = r; p = z (solver.hpp:109,123)
+          w1[g] = dv ? DD(r, dv[g]) : r;  // z = r / diag (or r); p = z (solver.hpp:105-109,123)
           pr = DM(r, r);
         } else {
           const double r = DS(x, DM(alpha, y));  // r -= alpha * Ap (solver.hpp:133)
@@ -155,6 +160,13 @@ __device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, d
       sc->pAp = tot;
       sc->alpha = sc->rz / tot;
     }
+  } else if (op == OP_RZ) {
+    if (sc->iterations == 0) {
+      sc->rz = tot;  // rz = r0.z0 (solver.hpp:124)
+    } else {
+      sc->beta = tot / sc->rz;  // solver.hpp:145-147
+      sc->rz = tot;
+    }
   } else if (op == OP_INIT) {
     const double r0 = sqrt(tot);
     hist[0] = r0;
@@ -178,18 +190,21 @@ __device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, d
     } else if (rnorm / sc->r0 <= sc->rel_tol) {
       sc->status = ST_CONVERGED;
     } else {
-      sc->beta = tot / sc->rz;
-      sc->rz = tot;
+      if (!sc->precond) {  // Jacobi: beta from OP_RZ
+        sc->beta = tot / sc->rz;
+        sc->rz = tot;
+      }
       if (k >= sc->max_iter) sc->status = ST_MAXITER;
     }
   }
 }
 
-// x += alpha p; p = r + beta p (solver.hpp:132,147), reference arithmetic.
+// x += alpha p; p = z + beta p, z = r / diag or r (solver.hpp:105-108,132,147).
 template <bool EXACT>
 __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x, double* __restrict__ p,
                                                           const double* __restrict__ r, long long n,
-                                                          unsigned int* done, DevScalars* sc) {
+                                                          unsigned int* done, DevScalars* sc,
+                                                          const double* __restrict__ dv) {
   if (*(volatile int*)&sc->x_pending == 0) return;
   const double alpha = sc->alpha, beta = sc->beta;
   const bool update_p = *(volatile int*)&sc->status == ST_RUNNING;
@@ -203,6 +218,7 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
       pv[u] = p[i + u * stride];
       xv[u] = x[i + u * stride];
       rv[u] = update_p ? r[i + u * stride] : 0.0;
+      if (dv && update_p) rv[u] = EXACT ? DD(rv[u], dv[i + u * stride]) : rv[u] / dv[i + u * stride];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -217,12 +233,13 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
   }
   for (; i < n; i += stride) {
     const double pi = p[i];
+    const double zi = update_p ? (dv ? (EXACT ? DD(r[i], dv[i]) : r[i] / dv[i]) : r[i]) : 0.0;
     if (EXACT) {
       x[i] = DA(x[i], DM(alpha, pi));
-      if (update_p) p[i] = DA(r[i], DM(beta, pi));
+      if (update_p) p[i] = DA(zi, DM(beta, pi));
     } else {
       x[i] = fma(alpha, pi, x[i]);
-      if (update_p) p[i] = fma(beta, pi, r[i]);
+      if (update_p) p[i] = fma(beta, pi, zi);
     }
   }
   if (!last_block(done)) return;
@@ -242,27 +259,35 @@ __device__ __forceinline__ double tree_partials(const double* part, int nblk, do
 __global__ void __launch_bounds__(VT) fused_init_kernel(const double* __restrict__ b, const double* __restrict__ Ap,
                                                         double* __restrict__ r, double* __restrict__ p, long long n,
                                                         double* part, unsigned int* done, DevScalars* sc,
-                                                        double* hist, double rel_tol, int max_iter) {
+                                                        double* hist, double rel_tol, int max_iter,
+                                                        const double* __restrict__ dv) {
   __shared__ double red[VT / 32];
-  double acc = 0.0;
+  double acc = 0.0, acz = 0.0;
   const long long stride = static_cast<long long>(gridDim.x) * VT;
   for (long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x; i < n; i += stride) {
     const double v = b[i] - Ap[i];
     r[i] = v;
-    p[i] = v;
+    const double z = dv ? v / dv[i] : v;
+    p[i] = z;
     acc = fma(v, v, acc);
+    acz = fma(v, z, acz);
   }
   const double s = block_sum<VT>(acc, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  const double sz = dv ? block_sum<VT>(acz, red) : 0.0;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    part[gridDim.x + blockIdx.x] = sz;
+  }
   if (!last_block(done)) return;
   __threadfence();
   const double rr = tree_partials(part, gridDim.x, red);
+  const double rz = dv ? tree_partials(part + gridDim.x, gridDim.x, red) : rr;
   if (threadIdx.x == 0) {
     const double r0 = sqrt(rr);
     hist[0] = r0;
     sc->r0 = r0;
     sc->rnorm = r0;
-    sc->rz = rr;
+    sc->rz = rz;
     sc->rel_tol = rel_tol;
     sc->max_iter = max_iter;
     sc->iterations = 0;
@@ -283,6 +308,7 @@ struct RingUpdateArgs {
   const double* p;        // the applied vector (ConstrainedOperator rows: A p = p)
   const double* latY;     // ring partials (ring.cuh layout)
   const double* latX;
+  const double* dv;       // Jacobi diagonal (nullptr: plain CG)
   double* r;
   int nx, ny, Nx, Ny, Nz, constrained, bc_zlo, bc_zhi;
 };
@@ -296,7 +322,7 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
   const int lane = threadIdx.x & 31;
   const int rows = R.Ny * R.Nz;  // < 2^31 (n_L < 2^31 checked at setup)
   const LatLayout L(P, R.nx, R.ny);
-  double acc = 0.0;
+  double acc = 0.0, acz = 0.0;  // r.r and, with a Jacobi diagonal, r.z
   const int lmod = lane % P;
   for (int row = blockIdx.x * (VT / 32) + (threadIdx.x >> 5); row < rows; row += gridDim.x * (VT / 32)) {
     const int Z = row / R.Ny, Y = row - Z * R.Ny;
@@ -304,6 +330,7 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
     double* rr_ = R.r + static_cast<long long>(R.Nx) * row;
     const double* ap = R.Ap + static_cast<long long>(R.Nx) * row;
     const double* pp = R.p + static_cast<long long>(R.Nx) * row;
+    const double* dd = R.dv ? R.dv + static_cast<long long>(R.Nx) * row : nullptr;
     if (Y % P != 0) {
       // plain row: interior nodes read A p; x-face nodes X = fx*P sum the
       // (left, right) partial pair of latX (one 16-byte load)
@@ -338,6 +365,7 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
             const double v = fma(-alpha, a[u], rv[u]);
             rr_[X] = v;
             acc = fma(v, v, acc);
+            if (dd) acz = fma(v, v / dd[X], acz);
           }
         }
       }
@@ -382,16 +410,22 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
             const double v = fma(-alpha, a[u], rv[u]);
             rr_[X] = v;
             acc = fma(v, v, acc);
+            if (dd) acz = fma(v, v / dd[X], acz);
           }
         }
       }
     }
   }
   const double s = block_sum<VT>(acc, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  const double sz = R.dv ? block_sum<VT>(acz, red) : 0.0;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    part[gridDim.x + blockIdx.x] = sz;
+  }
   if (!last_block(done)) return;
   __threadfence();
   const double rr = tree_partials(part, gridDim.x, red);
+  const double rz = R.dv ? tree_partials(part + gridDim.x, gridDim.x, red) : rr;
   if (threadIdx.x == 0) {
     const double rnorm = sqrt(rr);
     const int k = sc->iterations + 1;
@@ -404,8 +438,8 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
     } else if (rnorm / sc->r0 <= sc->rel_tol) {
       sc->status = ST_CONVERGED;
     } else {
-      sc->beta = rr / sc->rz;
-      sc->rz = rr;
+      sc->beta = rz / sc->rz;  // solver.hpp:145-147 (rz = r.r without a preconditioner)
+      sc->rz = rz;
       if (k >= sc->max_iter) sc->status = ST_MAXITER;
     }
     *done = 0;
@@ -513,8 +547,9 @@ int wave_grid(K kernel, int64_t n) {
 }
 
 int64_t reduction_partials(int64_t n) {
+  // exact-mode chunk partials, or two partials per CTA of the fused kernels
   const int64_t nch = (n + CHUNK - 1) / CHUNK;
-  return nch > 148 * 8 ? nch : 148 * 8;
+  return nch > 2 * 148 * 8 ? nch : 2 * 148 * 8;
 }
 
 cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
@@ -522,10 +557,10 @@ cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, doub
   if (ws.exact) {
     blocked_reduce_kernel<OP_INIT><<<chunk_grid(n), VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials,
                                                                  ws.vec_done, ws.sc, ws.history, nullptr, rel_tol,
-                                                                 max_iter);
+                                                                 max_iter, -1, ws.diag);
   } else {
     fused_init_kernel<<<vec_grid(n), VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials, ws.vec_done, ws.sc,
-                                                  ws.history, rel_tol, max_iter);
+                                                  ws.history, rel_tol, max_iter, ws.diag);
   }
   return cudaGetLastError();
 }
@@ -533,6 +568,12 @@ cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, doub
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st) {
   blocked_reduce_kernel<OP_PAP><<<chunk_grid(n), VT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials,
                                                               ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st) {
+  blocked_reduce_kernel<OP_RZ><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.diag, nullptr, nullptr, n, ws.vec_partials,
+                                                             ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
   return cudaGetLastError();
 }
 
@@ -549,6 +590,7 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
   R.p = ws.p;
   R.latY = ws.lateral;
   R.latX = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
+  R.dv = ws.diag;
   R.r = ws.r;
   R.nx = s.dims[0];
   R.ny = s.dims[1];
@@ -580,9 +622,9 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
 
 cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st) {
   if (ws.exact)
-    cg_update_xp_kernel<true><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc);
+    cg_update_xp_kernel<true><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc, ws.diag);
   else
-    cg_update_xp_kernel<false><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc);
+    cg_update_xp_kernel<false><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc, ws.diag);
   return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@ constexpr int kMaxQ = kMaxP + 2;
 struct DevScalars {
   double rz, pAp, alpha, beta, r0, rnorm, rel_tol, pad0;
   int status, iterations, x_pending, max_iter;
+  int precond, pad1;  // precond: Jacobi z = r / diag (beta from r.z, not r.r)
 };
 enum : int { ST_RUNNING = 0, ST_CONVERGED = 1, ST_DIVERGED = 2, ST_MAXITER = 3 };
 
@@ -98,6 +99,7 @@ struct Workspace {
   int history_cap = 0;
   int vec_blocks = 0;
   int exact = 1;                  // reduction mode (cg.cu): 1 = reference order, 0 = fused
+  const double* diag = nullptr;   // Jacobi diagonal of the running solve (nullptr: no preconditioner)
   double* dot_result = nullptr;
   DevScalars* host_sc = nullptr;  // pinned mirror
 };
@@ -121,6 +123,11 @@ cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, doub
                            cudaStream_t st);
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained = 1);
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st);
+// Jacobi PCG: rz = r.(r / diag) (reference order); at init sets rz, after an
+// r-update sets beta = rz_next / rz (solver.hpp:105-108, 145-147)
+cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st);
+// ---- jacobi.cu: jacobi_diagonal (solver.hpp:155-205) in reference arithmetic
+cudaError_t launch_jacobi_diagonal(const Setup& s, int constrained, double* diag, cudaStream_t st);
 int64_t reduction_partials(int64_t n);
 cudaError_t launch_cgd_reduce(const Workspace& ws, int op, const double* b, int64_t n, int64_t owned, double* out,
                               cudaStream_t st);

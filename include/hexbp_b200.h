@@ -153,6 +153,9 @@ int hexbp_pcg(hexbp_setup_t s, hexbp_workspace_t ws, const double* b_dev, double
  * vector; synchronous. */
 int hexbp_jacobi_diagonal(hexbp_setup_t s, int constrained, double* diag_dev, void* stream);
 
+/* Same, into a HOST vector of l_size doubles. */
+int hexbp_jacobi_diagonal_host(hexbp_setup_t s, int constrained, double* diag);
+
 /* Same as hexbp_pcg with HOST b, x and diag (diag may be NULL). */
 int hexbp_pcg_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* b, double* x, const double* diag, int64_t n,
                    double rel_tol, int max_iter, int constrained, hexbp_cg_report* report, double* history);

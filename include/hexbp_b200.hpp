@@ -189,15 +189,17 @@ struct CGReport {  // solver.hpp:76-82
 
 namespace detail {
 inline CGReport run_cg(const OperatorHandle& op, int constrained, std::span<const double> b, std::vector<double>& x,
-                       double rel_tol, int max_iter) {
+                       double rel_tol, int max_iter, const std::vector<double>* diag = nullptr) {
   const auto t0 = std::chrono::steady_clock::now();
   if (x.size() != b.size()) throw std::invalid_argument("cg: x0 length mismatch");
+  if (diag && diag->size() != b.size()) throw std::invalid_argument("cg: diagonal length mismatch");
   if (max_iter < 0) throw std::invalid_argument("cg: max_iter must be >= 0");
   CGReport r;
   std::vector<double> hist(static_cast<std::size_t>(max_iter) + 1);
   hexbp_cg_report rep{};
-  check(hexbp_cg_host(op.setup().handle(), op.workspace().handle(), b.data(), x.data(),
-                      static_cast<int64_t>(b.size()), rel_tol, max_iter, constrained, &rep, hist.data()));
+  check(hexbp_pcg_host(op.setup().handle(), op.workspace().handle(), b.data(), x.data(),
+                       diag ? diag->data() : nullptr, static_cast<int64_t>(b.size()), rel_tol, max_iter, constrained,
+                       &rep, hist.data()));
   r.iterations = rep.iterations;
   r.converged = rep.converged != 0;
   r.final_rel_residual = rep.final_rel_residual;
@@ -208,15 +210,27 @@ inline CGReport run_cg(const OperatorHandle& op, int constrained, std::span<cons
 }
 }  // namespace detail
 
-// cg (solver.hpp:91-153) for device operators: the recurrence runs on the device.
+// cg (solver.hpp:91-153) for device operators: the recurrence runs on the
+// device; `diag` = Jacobi preconditioner (solver.hpp:105-108), as the reference.
 inline CGReport cg(const OperatorHandle& op, std::span<const double> b, std::vector<double>& x, double rel_tol = 1e-8,
-                   int max_iter = 2000) {
-  return detail::run_cg(op, 0, b, x, rel_tol, max_iter);
+                   int max_iter = 2000, const std::vector<double>* diag = nullptr) {
+  return detail::run_cg(op, 0, b, x, rel_tol, max_iter, diag);
 }
 inline CGReport cg(const ConstrainedOperator& op, std::span<const double> b, std::vector<double>& x,
-                   double rel_tol = 1e-8, int max_iter = 2000) {
-  return detail::run_cg(op.raw(), 1, b, x, rel_tol, max_iter);
+                   double rel_tol = 1e-8, int max_iter = 2000, const std::vector<double>* diag = nullptr) {
+  return detail::run_cg(op.raw(), 1, b, x, rel_tol, max_iter, diag);
 }
+
+// jacobi_diagonal (solver.hpp:155-205), computed on the device, bit for bit.
+namespace detail {
+inline std::vector<double> jacobi(const OperatorHandle& op, int constrained) {
+  std::vector<double> out(static_cast<std::size_t>(op.size()));
+  check(hexbp_jacobi_diagonal_host(op.setup().handle(), constrained, out.data()));
+  return out;
+}
+}  // namespace detail
+inline std::vector<double> jacobi_diagonal(const OperatorHandle& op) { return detail::jacobi(op, 0); }
+inline std::vector<double> jacobi_diagonal(const ConstrainedOperator& op) { return detail::jacobi(op.raw(), 1); }
 
 // run_bench's right-hand side (bench.hpp:234-243), BENCH_SEED default 20240101
 inline std::vector<double> bench_rhs(BPKind kind, int p, std::array<int, 3> dims, uint64_t seed = 20240101ull) {

@@ -421,6 +421,21 @@ int hexbp_jacobi_diagonal(hexbp_setup_t h, int constrained, double* diag, void* 
   return HEXBP_OK;
 }
 
+int hexbp_jacobi_diagonal_host(hexbp_setup_t h, int constrained, double* diag) {
+  if (!h || !diag) return invalid("jacobi_diagonal: null argument");
+  DeviceGuard g(h->s.device);
+  double* d = nullptr;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(h->s.nL);
+  if (cudaMalloc(&d, bytes) != cudaSuccess) return cuda_status(cudaErrorMemoryAllocation, "jacobi_diagonal");
+  int rc = hexbp_jacobi_diagonal(h, constrained, d, nullptr);
+  if (rc == HEXBP_OK) {
+    const cudaError_t e = cudaMemcpy(diag, d, bytes, cudaMemcpyDeviceToHost);
+    if (e) rc = cuda_status(e, "jacobi_diagonal: copy");
+  }
+  cudaFree(d);
+  return rc;
+}
+
 int hexbp_pcg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, int64_t n,
                    double rel_tol, int max_iter, int constrained, hexbp_cg_report* report, double* history) {
   if (!h || !wh || !b || !x) return invalid("cg: null argument");

@@ -68,6 +68,13 @@ int main() {
     threw = true;
   }
   EXPECT(threw, "inverted element throws degenerate_element_error (geometry.hpp:129)");
+  // Jacobi-preconditioned cg (solver.hpp:91-205): reference run 202 iterations,
+  // final 9.155462415450827e-09 -- reproduced bit for bit in reference mode
+  const std::vector<double> diag = jacobi_diagonal(cop);
+  std::vector<double> xj(b.size(), 0.0);
+  const CGReport rj = cg(cop, b, xj, 1e-8, 2000, &diag);
+  EXPECT(rj.iterations == 202 && rj.converged, "pcg iterations %d (reference 202)", rj.iterations);
+  EXPECT(rj.final_rel_residual == 9.155462415450827e-09, "pcg final rel residual %.17g", rj.final_rel_residual);
   // fast mode: same iteration count within one, tolerance-level agreement
   op.workspace().set_mode(Mode::Fast);
   std::vector<double> x2(b.size(), 0.0);

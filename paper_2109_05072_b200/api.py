@@ -480,9 +480,14 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
                 raise ValueError("cg: diagonal length mismatch")  # solver.hpp:97
             _check_device_vec(diag, n, "cg")
             dptr = C.c_void_p(diag.data_ptr())
-        rc = _lib.lib().hexbp_pcg(op.setup()._h, ws._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), dptr,
-                                  rel_tol, max_iter, constrained, C.byref(rep), hist.ctypes.data_as(_dp),
-                                  _stream_ptr(b))
+        if dptr is None:
+            rc = _lib.lib().hexbp_cg(op.setup()._h, ws._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()),
+                                     rel_tol, max_iter, constrained, C.byref(rep), hist.ctypes.data_as(_dp),
+                                     _stream_ptr(b))
+        else:
+            rc = _lib.lib().hexbp_pcg(op.setup()._h, ws._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()),
+                                      dptr, rel_tol, max_iter, constrained, C.byref(rep), hist.ctypes.data_as(_dp),
+                                      _stream_ptr(b))
     else:
         b = np.ascontiguousarray(b, np.float64)
         if not isinstance(x, np.ndarray) or x.dtype != np.float64 or x.size != n or not x.flags.c_contiguous:

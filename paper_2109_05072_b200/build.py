@@ -60,7 +60,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp"]
+    link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xlinker", "--no-undefined", *objs,
+            "-o", LIB + ".tmp"]
     subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

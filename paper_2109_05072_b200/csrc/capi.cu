@@ -489,9 +489,14 @@ int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x,
       cudaMemsetAsync(reinterpret_cast<char*>(w.sc) + offsetof(DevScalars, precond), 0, sizeof(int), st);
     }
   } clear_diag{w, st};
-  // r0 = b - A x0 (solver.hpp:102-103)
-  CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
-  CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
+  // r0 = b - A x0 (solver.hpp:102-103); fast mode sums the ring in the init kernel
+  if (w.exact) {
+    CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
+    CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
+  } else {
+    CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st, /*finish_ring=*/false));
+    CK(launch_cg_init_ring(w, b, x, n, rel_tol, max_iter, constrained, st));
+  }
   if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz = r0.z0 (solver.hpp:124)
   const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
   for (int k = 1; k <= max_iter; ++k) {

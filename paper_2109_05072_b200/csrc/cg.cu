@@ -200,7 +200,7 @@ __device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, d
 }
 
 // x += alpha p; p = z + beta p, z = r / diag or r (solver.hpp:105-108,132,147).
-template <bool EXACT>
+template <bool EXACT, bool PC>
 __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x, double* __restrict__ p,
                                                           const double* __restrict__ r, long long n,
                                                           unsigned int* done, DevScalars* sc,
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
       pv[u] = p[i + u * stride];
       xv[u] = x[i + u * stride];
       rv[u] = update_p ? r[i + u * stride] : 0.0;
-      if (dv && update_p) rv[u] = EXACT ? DD(rv[u], dv[i + u * stride]) : rv[u] / dv[i + u * stride];
+      if (PC && update_p) rv[u] = EXACT ? DD(rv[u], dv[i + u * stride]) : rv[u] / dv[i + u * stride];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
   }
   for (; i < n; i += stride) {
     const double pi = p[i];
-    const double zi = update_p ? (dv ? (EXACT ? DD(r[i], dv[i]) : r[i] / dv[i]) : r[i]) : 0.0;
+    const double zi = update_p ? (PC ? (EXACT ? DD(r[i], dv[i]) : r[i] / dv[i]) : r[i]) : 0.0;
     if (EXACT) {
       x[i] = DA(x[i], DM(alpha, pi));
       if (update_p) p[i] = DA(zi, DM(beta, pi));
@@ -309,16 +309,22 @@ struct RingUpdateArgs {
   const double* latY;     // ring partials (ring.cuh layout)
   const double* latX;
   const double* dv;       // Jacobi diagonal (nullptr: plain CG)
+  const double* b;        // INIT: right-hand side (r = b - A x)
+  double* pout;           // INIT: p = z
+  double rel_tol;         // INIT: stopping rule parameters
+  int max_iter;
   double* r;
   int nx, ny, Nx, Ny, Nz, constrained, bc_zlo, bc_zhi;
 };
 
-template <int P>
+// INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
+// r.r -> r0 and the stopping state, r.z -> rz (solver.hpp:102-124).
+template <int P, bool INIT, bool PC>
 __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_constant__ RingUpdateArgs R, double* part,
                                                                  unsigned int* done, DevScalars* sc, double* hist) {
   __shared__ double red[VT / 32];
-  if (*(volatile int*)&sc->status != ST_RUNNING) return;
-  const double alpha = sc->alpha;
+  if (!INIT && *(volatile int*)&sc->status != ST_RUNNING) return;
+  const double alpha = INIT ? 0.0 : sc->alpha;
   const int lane = threadIdx.x & 31;
   const int rows = R.Ny * R.Nz;  // < 2^31 (n_L < 2^31 checked at setup)
   const LatLayout L(P, R.nx, R.ny);
@@ -330,7 +336,9 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
     double* rr_ = R.r + static_cast<long long>(R.Nx) * row;
     const double* ap = R.Ap + static_cast<long long>(R.Nx) * row;
     const double* pp = R.p + static_cast<long long>(R.Nx) * row;
-    const double* dd = R.dv ? R.dv + static_cast<long long>(R.Nx) * row : nullptr;
+    const double* dd = PC ? R.dv + static_cast<long long>(R.Nx) * row : nullptr;
+    const double* bb = INIT ? R.b + static_cast<long long>(R.Nx) * row : nullptr;
+    double* po = INIT ? R.pout + static_cast<long long>(R.Nx) * row : nullptr;
     if (Y % P != 0) {
       // plain row: interior nodes read A p; x-face nodes X = fx*P sum the
       // (left, right) partial pair of latX (one 16-byte load)
@@ -362,10 +370,12 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
         for (int u = 0; u < 4; ++u) {
           const int X = x0 + 32 * u + lane;
           if (X < R.Nx) {
-            const double v = fma(-alpha, a[u], rv[u]);
+            const double v = INIT ? bb[X] - a[u] : fma(-alpha, a[u], rv[u]);
             rr_[X] = v;
             acc = fma(v, v, acc);
-            if (dd) acz = fma(v, v / dd[X], acz);
+            const double z = PC ? v / dd[X] : v;
+            if (PC) acz = fma(v, z, acz);
+            if (INIT) po[X] = z;
           }
         }
       }
@@ -407,25 +417,44 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
         for (int u = 0; u < 2; ++u) {
           const int X = x0 + 32 * u + lane;
           if (X < R.Nx) {
-            const double v = fma(-alpha, a[u], rv[u]);
+            const double v = INIT ? bb[X] - a[u] : fma(-alpha, a[u], rv[u]);
             rr_[X] = v;
             acc = fma(v, v, acc);
-            if (dd) acz = fma(v, v / dd[X], acz);
+            const double z = PC ? v / dd[X] : v;
+            if (PC) acz = fma(v, z, acz);
+            if (INIT) po[X] = z;
           }
         }
       }
     }
   }
   const double s = block_sum<VT>(acc, red);
-  const double sz = R.dv ? block_sum<VT>(acz, red) : 0.0;
+  const double sz = PC ? block_sum<VT>(acz, red) : 0.0;
   if (threadIdx.x == 0) {
     part[blockIdx.x] = s;
-    part[gridDim.x + blockIdx.x] = sz;
+    if (PC) part[gridDim.x + blockIdx.x] = sz;
   }
   if (!last_block(done)) return;
   __threadfence();
   const double rr = tree_partials(part, gridDim.x, red);
-  const double rz = R.dv ? tree_partials(part + gridDim.x, gridDim.x, red) : rr;
+  const double rz = PC ? tree_partials(part + gridDim.x, gridDim.x, red) : rr;
+  if (INIT) {
+    if (threadIdx.x == 0) {
+      const double r0 = sqrt(rr);
+      hist[0] = r0;
+      sc->r0 = r0;
+      sc->rnorm = r0;
+      sc->rz = rz;
+      sc->rel_tol = R.rel_tol;
+      sc->max_iter = R.max_iter;
+      sc->iterations = 0;
+      sc->x_pending = 0;
+      sc->status = !isfinite(r0) ? ST_DIVERGED
+                                 : (r0 == 0.0 ? ST_CONVERGED : (R.max_iter <= 0 ? ST_MAXITER : ST_RUNNING));
+      *done = 0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     const double rnorm = sqrt(rr);
     const int k = sc->iterations + 1;
@@ -577,20 +606,21 @@ cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained) {
-  if (ws.exact) {
-    blocked_reduce_kernel<OP_UPDATE_R><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
-                                                                     ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
-    return cudaGetLastError();
-  }
-  // fast mode: A p comes from launch_apply(..., finish_ring = false)
+namespace {
+template <bool INIT>
+cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained, const double* p_applied,
+                          const double* b, double rel_tol, int max_iter) {
   const Setup& s = *ws.s;
   RingUpdateArgs R;
   R.Ap = ws.Ap;
-  R.p = ws.p;
+  R.p = p_applied;
   R.latY = ws.lateral;
   R.latX = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
   R.dv = ws.diag;
+  R.b = b;
+  R.pout = ws.p;
+  R.rel_tol = rel_tol;
+  R.max_iter = max_iter;
   R.r = ws.r;
   R.nx = s.dims[0];
   R.ny = s.dims[1];
@@ -601,10 +631,14 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
   R.bc_zlo = s.bc_zlo;
   R.bc_zhi = s.bc_zhi;
   switch (s.p) {
-#define HXB_RING_CASE(PP)                                                                                         \
-  case PP:                                                                                                         \
-    fused_ring_update_r_kernel<PP><<<wave_grid(fused_ring_update_r_kernel<PP>, n), VT, 0, st>>>(                   \
-        R, ws.vec_partials, ws.vec_done, ws.sc, ws.history);                                                       \
+#define HXB_RING_CASE(PP)                                                                                             \
+  case PP:                                                                                                             \
+    if (R.dv)                                                                                                          \
+      fused_ring_update_r_kernel<PP, INIT, true><<<wave_grid(fused_ring_update_r_kernel<PP, INIT, true>, n), VT, 0,     \
+                                                   st>>>(R, ws.vec_partials, ws.vec_done, ws.sc, ws.history);          \
+    else                                                                                                               \
+      fused_ring_update_r_kernel<PP, INIT, false><<<wave_grid(fused_ring_update_r_kernel<PP, INIT, false>, n), VT, 0,   \
+                                                    st>>>(R, ws.vec_partials, ws.vec_done, ws.sc, ws.history);         \
     break;
     HXB_RING_CASE(1)
     HXB_RING_CASE(2)
@@ -619,12 +653,37 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
   }
   return cudaGetLastError();
 }
+}  // namespace
 
-cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st) {
-  if (ws.exact)
-    cg_update_xp_kernel<true><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc, ws.diag);
-  else
-    cg_update_xp_kernel<false><<<vec_grid(n), VT, 0, st>>>(x, ws.p, ws.r, n, ws.vec_done, ws.sc, ws.diag);
+cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained) {
+  if (ws.exact) {
+    blocked_reduce_kernel<OP_UPDATE_R><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
+                                                                     ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
+    return cudaGetLastError();
+  }
+  // fast mode: A p comes from launch_apply(..., finish_ring = false)
+  return launch_ring_r<false>(ws, n, st, constrained, ws.p, nullptr, 0.0, 0);
+}
+
+cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const double* x, int64_t n, double rel_tol,
+                                int max_iter, int constrained, cudaStream_t st) {
+  return launch_ring_r<true>(ws, n, st, constrained, x, b, rel_tol, max_iter);
+}
+
+cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st, double* p) {
+  if (!p) p = ws.p;
+  const int g = vec_grid(n);
+  if (ws.exact) {
+    if (ws.diag)
+      cg_update_xp_kernel<true, true><<<g, VT, 0, st>>>(x, p, ws.r, n, ws.vec_done, ws.sc, ws.diag);
+    else
+      cg_update_xp_kernel<true, false><<<g, VT, 0, st>>>(x, p, ws.r, n, ws.vec_done, ws.sc, nullptr);
+  } else {
+    if (ws.diag)
+      cg_update_xp_kernel<false, true><<<g, VT, 0, st>>>(x, p, ws.r, n, ws.vec_done, ws.sc, ws.diag);
+    else
+      cg_update_xp_kernel<false, false><<<g, VT, 0, st>>>(x, p, ws.r, n, ws.vec_done, ws.sc, nullptr);
+  }
   return cudaGetLastError();
 }
 

@@ -123,6 +123,9 @@ cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, doub
                            cudaStream_t st);
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained = 1);
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st);
+// fast mode: r = b - A x with A x from launch_apply(x, ..., finish_ring = false)
+cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const double* x, int64_t n, double rel_tol,
+                                int max_iter, int constrained, cudaStream_t st);
 // Jacobi PCG: rz = r.(r / diag) (reference order); at init sets rz, after an
 // r-update sets beta = rz_next / rz (solver.hpp:105-108, 145-147)
 cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st);
@@ -135,7 +138,7 @@ cudaError_t launch_cgd_finish(const Workspace& ws, int op, const double* gathere
                               int max_iter, cudaStream_t st);
 cudaError_t launch_plane_combine(double* dst, const double* src, const double* u, int nxn, int nyn, int constrained,
                                  cudaStream_t st);
-cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st);
+cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st, double* p = nullptr);
 cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
                        cudaStream_t st);
 int vec_grid(int64_t n);

@@ -600,12 +600,15 @@ bool use_mma(const Setup& s) {
     return v && *v && *v != '0';
   }();
   // the [qp][6] factor layout of BP3 p=7 setups is read by the DMMA kernel only
-  return (s.g_aos || !disabled) && mma_kernel_applies(s);
+  return (s.g_aos || !disabled) && (mma_kernel_applies(s) || mma5_kernel_applies(s));
 }
 
 void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm) {
   if (use_mma(s)) {
-    mma_kernel_info(regs, smem, threads, blocks_per_sm);
+    if (mma5_kernel_applies(s))
+      mma5_kernel_info(regs, smem, threads, blocks_per_sm);
+    else
+      mma_kernel_info(regs, smem, threads, blocks_per_sm);
     return;
   }
   const KInfo ki = info_for(s);
@@ -649,7 +652,7 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   }
   cudaError_t e = cudaErrorInvalidValue;
   if (use_mma(s)) {
-    e = launch_apply_mma(s, a, st);
+    e = mma5_kernel_applies(s) ? launch_apply_mma5(s, a, st) : launch_apply_mma(s, a, st);
   } else {
     switch (s.kind) {
       case KIND_MASS: e = launch_k<KIND_MASS>(s, a, st); break;

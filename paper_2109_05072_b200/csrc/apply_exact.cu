@@ -367,9 +367,10 @@ __global__ void __launch_bounds__(XCfg<P, Q, KIND>::NT, 1)
           double u = 0.0;
           for (int k = 0; k < N; ++k) u = DA(u, DM(bs.D[c][k], x[k]));
           const double r = T1[at(a, b, c)], s = T2[at(a, b, c)];
-          const double* g = Gs + a * N * N + b + N * c;
-          const double g0 = g[0], g1 = g[N * N * N], g2 = g[2 * N * N * N], g3 = g[3 * N * N * N],
-                       g4 = g[4 * N * N * N], g5 = g[5 * N * N * N];
+          // factor layout: [m][a][b + q c] (0) or [c][m][b][a] (2, BP5 p=7 DMMA setups)
+          const double* g = A.g_aos == 2 ? Gs + (c * 6 * N + b) * N + a : Gs + a * N * N + b + N * c;
+          const int cs = A.g_aos == 2 ? N * N : N * N * N;  // component stride
+          const double g0 = g[0], g1 = g[cs], g2 = g[2 * cs], g3 = g[3 * cs], g4 = g[4 * cs], g5 = g[5 * cs];
           T1[at(a, b, c)] = DA(DA(DM(g0, r), DM(g1, s)), DM(g2, u));
           T2[at(a, b, c)] = DA(DA(DM(g1, r), DM(g3, s)), DM(g4, u));
           vt[c] = DA(DA(DM(g2, r), DM(g4, s)), DM(g5, u));

@@ -97,7 +97,8 @@ int init_setup(Setup& s, int bp, int p, const int gdims[3], int z0, int z1, int 
   s.E = static_cast<int64_t>(s.dims[0]) * s.dims[1] * s.dims[2];
   const long long per = static_cast<long long>(s.comp) * s.q * s.q * s.q;
   s.gstride = (per + 1) / 2 * 2;
-  s.g_aos = (s.kind == KIND_DIFF && p == 7) ? 1 : 0;  // DMMA kernel reads [qp][6] (apply_mma.cu)
+  // DMMA kernels' factor block orders: [qp][6] (BP3 p=7, apply_mma.cu), [c][6][b][a] (BP5 p=7, apply_mma5.cu)
+  s.g_aos = (s.kind == KIND_DIFF && p == 7) ? 1 : ((s.kind == KIND_COLLOC && p == 7) ? 2 : 0);
   std::vector<double> qp(s.q), npn(p + 1), nw(p + 1);
   try {
     build_basis(p, s.q, bp == 5, s.B, s.D, qp.data(), s.qw, npn.data(), nw.data());

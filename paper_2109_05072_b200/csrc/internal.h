@@ -112,6 +112,10 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
 int fixup_grid(const Setup& s);
 // ---- apply_mma.cu (FP64 tensor-core kernel, BP3 p = 7)
 bool mma_kernel_applies(const Setup& s);
+// ---- apply_mma5.cu (FP64 tensor-core kernel, BP5 p = 7)
+bool mma5_kernel_applies(const Setup& s);
+cudaError_t launch_apply_mma5(const Setup& s, const ApplyArgs& a, cudaStream_t st);
+void mma5_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm);
 cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st);
 void mma_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm);
 // ---- apply_exact.cu (bit-exact reference arithmetic)

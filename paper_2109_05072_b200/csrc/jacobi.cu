@@ -44,8 +44,9 @@ __global__ void jacobi_elem_kernel(const JacCfg c, const double* __restrict__ G,
   for (int t = threadIdx.x; t < q3 * c.comp; t += blockDim.x) {
     const int qp = t / c.comp, m = t - qp * c.comp;
     const int a = qp % q, b = (qp / q) % q, cc = qp / (q * q);
-    const long long off = c.aos ? static_cast<long long>(qp) * c.comp + m
-                                : static_cast<long long>(m) * q3 + static_cast<long long>(a) * q * q + (b + q * cc);
+    const long long off = c.aos == 2 ? ((static_cast<long long>(cc) * c.comp + m) * q + b) * q + a
+                          : c.aos    ? static_cast<long long>(qp) * c.comp + m
+                                     : static_cast<long long>(m) * q3 + static_cast<long long>(a) * q * q + (b + q * cc);
     g[t] = Ge[off];
   }
   __syncthreads();

@@ -16,6 +16,9 @@
 //   i.e. component m, then the x-index a of the point, then the (y,z) pair,
 //   so the x-pencil thread (b,c) of the kernel reads coalesced rows.
 //   Slot stride gstride = comp*q^3 rounded up to an even count (16 B).
+// The DMMA kernels use their own element-block orders (Setup::g_aos):
+//   1 = [qp][comp] (BP3 p=7, apply_mma.cu), 2 = [c][comp][b][a] (BP5 p=7,
+//   apply_mma5.cu: one z-plane of all components is a contiguous block).
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -36,7 +39,8 @@ struct GeomCfg {
 // Offset of component m of quadrature point (a, b, c) inside an element block.
 __device__ __forceinline__ long long gidx(const GeomCfg& cfg, int m, int a, int b, int c) {
   const int q = cfg.q;
-  if (cfg.aos) return static_cast<long long>(a + q * (b + q * c)) * cfg.comp + m;  // [qp][comp]
+  if (cfg.aos == 2) return ((static_cast<long long>(c) * cfg.comp + m) * q + b) * q + a;  // [c][comp][b][a]
+  if (cfg.aos) return static_cast<long long>(a + q * (b + q * c)) * cfg.comp + m;           // [qp][comp]
   return static_cast<long long>(m) * q * q * q + static_cast<long long>(a) * q * q + (b + q * c);
 }
 

@@ -361,20 +361,25 @@ def main():
     torch.cuda.empty_cache()
     if not args.no_sweep:
         line["p_sweep"] = p_sweep(bp, K, local)
+        # BASELINE configs[1]: BP1 mass operator, p = 1..8, ~10M DOFs; and the
+        # BP5 (collocated) operator of configs[3] at p = 7 on one GPU
+        line["bp1_sweep_10M"] = p_sweep(1, K, local, ps=tuple(range(1, 9)), dofs=10_000_000)
+        line["bp5_p7_50M"] = p_sweep(5, K, local, ps=(7,))
     print(json.dumps(line), flush=True)
 
 
-def p_sweep(bp: int, K: int, local: int):
-    """GDOF/s vs p (the metric is quoted 'vs p') at ~50M DOFs per GPU."""
+def p_sweep(bp: int, K: int, local: int, ps=(2, 3, 4, 5, 6, 8), dofs: float = 50_000_000):
+    """GDOF/s vs p (the metric is quoted 'vs p') at ~`dofs` DOFs per GPU,
+    fixed-iteration fast CG timed with CUDA events."""
     import torch
 
     import paper_2109_05072_b200 as hx
 
     out = {}
     peak, _ = load_peaks()
-    for p in (2, 3, 4, 5, 6, 8):
+    for p in ps:
         e = 1
-        while ((e + 1) * p + 1) ** 3 <= 50_000_000:
+        while ((e + 1) * p + 1) ** 3 <= dofs:
             e += 1
         dims = (e, e, e)
         try:

@@ -205,6 +205,9 @@ int ref_pcg(void* hv, int constrained, const double* b, double* x, const double*
   }
 }
 
+// kCsvHeader (bench.hpp:297-299): the CSV schema the harness mirror must keep.
+const char* ref_csv_header() { return kCsvHeader; }
+
 // run_bench through the reference's JSON config parser (bench.hpp:93-153,
 // 214-295). Writes up to `cap` records: throughput (dofs*iters/s), seconds,
 // dofs, threads. Returns the record count, or -1 on error (see ref_last_error).

@@ -107,6 +107,17 @@ void hexbp_workspace_destroy(hexbp_workspace_t ws);
  *    reproducible run to run, iterates equal to the reference's up to
  *    rounding. hexbp_dot always uses the reference order. */
 enum { HEXBP_MODE_REFERENCE = 0, HEXBP_MODE_FAST = 1 };
+
+/* Operator backend of a workspace (Backend, operator.hpp:31):
+ *  HEXBP_BACKEND_FUSED (default): one fused kernel per apply (Backend::Fused).
+ *  HEXBP_BACKEND_MULTIPASS: OperatorHandle::apply_multipass (operator.hpp:
+ *    318-394) on the GPU -- gather, gradient pass, factor pass, transpose
+ *    pass, scatter_add, with the E-vectors and quadrature fields in HBM (the
+ *    cuda-ref analog); always in reference arithmetic (bit
+ *    for bit the reference's Multipass). Allocates 2 E (p+1)^3 + 6 E q^3
+ *    doubles here (apply never allocates). */
+enum { HEXBP_BACKEND_FUSED = 0, HEXBP_BACKEND_MULTIPASS = 1 };
+int hexbp_workspace_set_backend(hexbp_workspace_t ws, int backend);
 int hexbp_workspace_set_mode(hexbp_workspace_t ws, int mode);
 
 /* Replaces OperatorHandle::apply(u, w, ws) (operator.hpp:265-279) and, with

@@ -208,9 +208,14 @@ class RefLib(Oracle):
     prefix = "ref_"
     so = REF_SO
 
-    def _create(self, bp, p, dims, a, backend: int = 1):
+    def __init__(self, bp: int, p: int, dims, amplitude: float = 0.0, backend: int = 1):
+        """backend: 1 = Backend::Fused, 0 = Backend::Multipass (operator.hpp:31)."""
+        self.backend = backend
+        super().__init__(bp, p, dims, amplitude)
+
+    def _create(self, bp, p, dims, a):
         self._fn("create").argtypes = [C.c_int] * 5 + [C.c_double, C.c_int]
-        return self._fn("create")(bp, p, dims[0], dims[1], dims[2], a, backend)
+        return self._fn("create")(bp, p, dims[0], dims[1], dims[2], a, getattr(self, "backend", 1))
 
     def _cg_extra(self):
         return [_dp]

@@ -62,6 +62,7 @@ def lib() -> C.CDLL:
         "hexbp_pcg_host": (C.c_int, [_vp, _vp, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_int, C.c_int,
                                      C.POINTER(CGReportC), _dp]),
         "hexbp_jacobi_diagonal": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+        "hexbp_workspace_set_backend": (C.c_int, [_vp, C.c_int]),
         "hexbp_jacobi_diagonal_host": (C.c_int, [_vp, C.c_int, _dp]),
         "hexbp_cg_host": (C.c_int, [_vp, _vp, _dp, _dp, C.c_int64, C.c_double, C.c_int, C.c_int,
                                     C.POINTER(CGReportC), _dp]),

@@ -82,7 +82,8 @@ class BPKind(enum.IntEnum):
 
 
 class Backend(enum.Enum):
-    Cuda = "cuda"
+    Cuda = "cuda"  # Backend::Fused on the GPU (fast or reference arithmetic, Workspace.set_mode)
+    CudaMultipass = "cuda-multipass"  # Backend::Multipass on the GPU (multipass.cu), reference arithmetic
 
 
 def to_string(v) -> str:
@@ -100,10 +101,11 @@ def parse_bp(s: str) -> BPKind:  # bench.hpp:80-85
     return m[s]
 
 
-def parse_backend(s: str) -> Backend:  # bench.hpp:86-91, plus the new "cuda" value
-    if s != "cuda":
-        raise ValueError(f"unknown backend '{s}' (this package provides: cuda)")
-    return Backend.Cuda
+def parse_backend(s: str) -> Backend:  # bench.hpp:86-91, with the CUDA backends' names
+    for b in Backend:
+        if b.value == s:
+            return b
+    raise ValueError(f"unknown backend '{s}' (this package provides: cuda, cuda-multipass)")
 
 
 def is_diffusion(k: BPKind) -> bool:  # operator.hpp:51
@@ -339,11 +341,11 @@ class OperatorHandle:
     """OperatorHandle (operator.hpp:244-420) bound to the CUDA backend."""
 
     def __init__(self, backend: Backend, setup: OperatorSetup):
-        if backend != Backend.Cuda:
-            raise ValueError("OperatorHandle: this package implements Backend.Cuda only")
+        if backend not in (Backend.Cuda, Backend.CudaMultipass):
+            raise ValueError("OperatorHandle: this package implements the CUDA backends only")
         self._backend = backend
         self._setup = setup
-        self._ws = Workspace(setup)
+        self._ws = self.make_workspace()
 
     def kind(self) -> BPKind:
         return self._setup.kind
@@ -358,7 +360,10 @@ class OperatorHandle:
         return self._setup.l_size()
 
     def make_workspace(self) -> Workspace:
-        return Workspace(self._setup)
+        ws = Workspace(self._setup)
+        if self._backend == Backend.CudaMultipass:
+            _check(_lib.lib().hexbp_workspace_set_backend(ws._h, 1))
+        return ws
 
     def workspace(self) -> Workspace:
         return self._ws
@@ -461,6 +466,8 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
     else:
         raise TypeError("cg: expected an OperatorHandle or ConstrainedOperator of the CUDA backend")
     ws = ws or op.workspace()
+    if op.backend() == Backend.CudaMultipass:
+        mode = "reference"  # the multipass pipeline runs in reference arithmetic
     ws.set_mode(mode)
     n = op.size()
     rep = _lib.CGReportC()

@@ -646,6 +646,10 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.fix_done = ws.fix_done;
   a.sc = sc;
   a.dot_out = dot_out;
+  if (ws.multipass) {  // Backend::Multipass analog (reference arithmetic; CG reduces in cg.cu)
+    if (dot_out || sc) return cudaErrorInvalidValue;
+    return launch_apply_multipass(s, ws.mp_buf, u, w, constrained, st);
+  }
   if (ws.exact) {
     if (dot_out || sc) return cudaErrorInvalidValue;  // the exact path reduces in cg.cu
     return launch_apply_exact(s, a, ws.fixup_grid, st);

@@ -367,7 +367,7 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   if (!wh) return;
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
-  void* bufs[] = {w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
+  void* bufs[] = {w.mp_buf, w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
                   w.vec_done, w.history, w.dot_result};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -637,7 +637,25 @@ int hexbp_plane_combine(double* dst, const double* src, const double* u, int nxn
 
 int hexbp_workspace_set_mode(hexbp_workspace_t wh, int mode) {
   if (!wh || (mode != HEXBP_MODE_REFERENCE && mode != HEXBP_MODE_FAST)) return invalid("bad arithmetic mode");
+  if (wh->w.multipass && mode == HEXBP_MODE_FAST)
+    return invalid("the multipass backend runs in reference arithmetic only");
   wh->w.exact = mode == HEXBP_MODE_REFERENCE;
+  return HEXBP_OK;
+}
+
+int hexbp_workspace_set_backend(hexbp_workspace_t wh, int backend) {
+  if (!wh || (backend != HEXBP_BACKEND_FUSED && backend != HEXBP_BACKEND_MULTIPASS)) return invalid("bad backend");
+  Workspace& w = wh->w;
+  DeviceGuard g(w.device);
+  if (backend == HEXBP_BACKEND_MULTIPASS && !w.mp_buf) {
+    const size_t bytes = sizeof(double) * static_cast<size_t>(multipass_doubles(*w.s));
+    if (cudaMalloc(&w.mp_buf, bytes) != cudaSuccess) {
+      w.mp_buf = nullptr;
+      return cuda_status(cudaErrorMemoryAllocation, "multipass workspace");
+    }
+  }
+  w.multipass = backend == HEXBP_BACKEND_MULTIPASS;
+  if (w.multipass) w.exact = 1;
   return HEXBP_OK;
 }
 

@@ -100,6 +100,8 @@ struct Workspace {
   int vec_blocks = 0;
   int exact = 1;                  // reduction mode (cg.cu): 1 = reference order, 0 = fused
   const double* diag = nullptr;   // Jacobi diagonal of the running solve (nullptr: no preconditioner)
+  int multipass = 0;              // HEXBP_BACKEND_MULTIPASS (multipass.cu)
+  double* mp_buf = nullptr;       // its E-vectors, quadrature fields and basis tables
   double* dot_result = nullptr;
   DevScalars* host_sc = nullptr;  // pinned mirror
 };
@@ -133,6 +135,10 @@ cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const doub
 // Jacobi PCG: rz = r.(r / diag) (reference order); at init sets rz, after an
 // r-update sets beta = rz_next / rz (solver.hpp:105-108, 145-147)
 cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st);
+// ---- multipass.cu: apply_multipass (operator.hpp:318-394) on the GPU
+int64_t multipass_doubles(const Setup& s);
+cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u, double* w, int constrained,
+                                   cudaStream_t st);
 // ---- jacobi.cu: jacobi_diagonal (solver.hpp:155-205) in reference arithmetic
 cudaError_t launch_jacobi_diagonal(const Setup& s, int constrained, double* diag, cudaStream_t st);
 int64_t reduction_partials(int64_t n);

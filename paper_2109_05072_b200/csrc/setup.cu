@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "tensor_dev.cuh"
 
 namespace hxb {
 namespace {
@@ -44,57 +45,7 @@ __device__ __forceinline__ long long gidx(const GeomCfg& cfg, int m, int a, int 
   return static_cast<long long>(m) * q * q * q + static_cast<long long>(a) * q * q + (b + q * c);
 }
 
-// contract_dim (tensor.hpp:50-114), all threads of the CTA cooperate; each
-// output entry is produced by one thread with the reference's summation order.
-__device__ void contract_dim_dev(const double* A, int m, int n, int axis, const double* x, int n0, int n1, int n2,
-                                 double* y, bool accumulate) {
-  if (axis == 0) {
-    const int rest = n1 * n2;
-    for (int o = threadIdx.x; o < rest * m; o += blockDim.x) {
-      const int c = o / m, a = o % m;
-      double sum = 0.0;
-      for (int i = 0; i < n; ++i) sum = DA(sum, DM(A[a * n + i], x[c * n0 + i]));
-      y[c * m + a] = accumulate ? DA(y[c * m + a], sum) : sum;
-    }
-  } else if (axis == 1) {
-    for (int o = threadIdx.x; o < n2 * m * n0; o += blockDim.x) {
-      const int i = o % n0, a = (o / n0) % m, k = o / (n0 * m);
-      double* yp = y + k * n0 * m + a * n0 + i;
-      double v = accumulate ? *yp : 0.0;
-      for (int j = 0; j < n; ++j) v = DA(v, DM(A[a * n + j], x[k * n0 * n1 + j * n0 + i]));
-      *yp = v;
-    }
-  } else {
-    const int plane = n0 * n1;
-    for (int o = threadIdx.x; o < m * plane; o += blockDim.x) {
-      const int i = o % plane, a = o / plane;
-      double* yp = y + a * plane + i;
-      double v = accumulate ? *yp : 0.0;
-      for (int k = 0; k < n; ++k) v = DA(v, DM(A[a * n + k], x[k * plane + i]));
-      *yp = v;
-    }
-  }
-  __syncthreads();
-}
-
-// elem_grad (tensor.hpp:177-203).
-__device__ void elem_grad_dev(const double* B, const double* D, int n, int q, bool colloc, const double* u,
-                              double* gr, double* gs, double* gt, double* ta, double* tb) {
-  if (colloc) {
-    contract_dim_dev(D, q, n, 0, u, n, n, n, gr, false);
-    contract_dim_dev(D, q, n, 1, u, n, n, n, gs, false);
-    contract_dim_dev(D, q, n, 2, u, n, n, n, gt, false);
-    return;
-  }
-  contract_dim_dev(D, q, n, 0, u, n, n, n, ta, false);
-  contract_dim_dev(B, q, n, 1, ta, q, n, n, tb, false);
-  contract_dim_dev(B, q, n, 2, tb, q, q, n, gr, false);
-  contract_dim_dev(B, q, n, 0, u, n, n, n, ta, false);
-  contract_dim_dev(D, q, n, 1, ta, q, n, n, tb, false);
-  contract_dim_dev(B, q, n, 2, tb, q, q, n, gs, false);
-  contract_dim_dev(B, q, n, 1, ta, q, n, n, tb, false);
-  contract_dim_dev(D, q, n, 2, tb, q, q, n, gt, false);
-}
+using tdev::elem_grad_dev;
 
 __global__ void box_geometry_kernel(GeomCfg cfg, const double* __restrict__ Bg, const double* __restrict__ Dg,
                                     const double* __restrict__ qw, BoxGeometryArgs g, double* __restrict__ G,

@@ -11,7 +11,9 @@ Backends: the reference's names are accepted by the parser ("multipass",
 "fused", "oracle": CPU backends of the reference, not run here) plus
   "cuda"        -- the B200 path, fast mode (DMMA / FMA kernels, fused CG),
   "cuda-exact"  -- the B200 path in reference arithmetic (its residual
-                   histories equal the reference's fused backend bit for bit).
+                   histories equal the reference's fused backend bit for bit),
+  "cuda-multipass" -- the unfused five-pass pipeline on the GPU (multipass.cu,
+                   the paper's cuda-ref comparison point), reference arithmetic.
 Timing uses CUDA events around each device-resident solve.
 
     python -m paper_2109_05072_b200.harness config.json [--csv out.csv] [--plot out.dat]
@@ -31,7 +33,7 @@ K_MAX_DEFORM_AMPLITUDE = 0.15  # mesh.hpp:53
 CSV_HEADER = ("bp,backend,p,q,elements,dofs,cg_iters,seconds,throughput,"
               "model_flops_per_elem,model_reads_per_elem,model_ai,threads")
 CPU_BACKENDS = ("multipass", "fused", "oracle")
-GPU_BACKENDS = ("cuda", "cuda-exact")
+GPU_BACKENDS = ("cuda", "cuda-exact", "cuda-multipass")
 
 
 class ConfigError(RuntimeError):
@@ -138,7 +140,8 @@ def parse_config(j) -> BenchConfig:
         cfg.backends = []
         for b in j["backends"]:
             if b not in CPU_BACKENDS + GPU_BACKENDS:
-                raise ConfigError(f"unknown backend '{b}' (expected multipass, fused, oracle, cuda or cuda-exact)")
+                raise ConfigError(f"unknown backend '{b}' (expected multipass, fused, oracle, cuda, cuda-exact "
+                                  "or cuda-multipass)")
             cfg.backends.append(b)
         if not cfg.backends:
             raise ConfigError("'backends' must be non-empty")
@@ -206,7 +209,8 @@ def run_bench(config: BenchConfig, device: int = 0) -> RunOutput:
                     raise ConfigError(f"backend '{backend}' is a CPU backend of the reference (not run here)")
                 kind = BPKind({"bp1": 1, "bp3": 3, "bp5": 5}[config.bp])
                 mesh = build_box_mesh(dims, p, (1.0, 1.0, 1.0), config.deform_amplitude)
-                op = OperatorHandle(Backend.Cuda, make_setup(kind, mesh, device=device))
+                op = OperatorHandle(Backend.CudaMultipass if backend == "cuda-multipass" else Backend.Cuda,
+                                    make_setup(kind, mesh, device=device))
                 mode = "fast" if backend == "cuda" else "reference"
                 A = ConstrainedOperator(op) if kind != BPKind.BP1 else op
                 dev = torch.device("cuda", device)

@@ -365,6 +365,10 @@ def main():
         # BP5 (collocated) operator of configs[3] at p = 7 on one GPU
         line["bp1_sweep_10M"] = p_sweep(1, K, local, ps=tuple(range(1, 9)), dofs=10_000_000)
         line["bp5_p7_50M"] = p_sweep(5, K, local, ps=(7,))
+        # the paper's fusion comparison: fused single-kernel operator vs the
+        # five-pass (gather / grad / factor / grad^T / scatter) pipeline
+        line["fusion_vs_multipass"] = {f"bp{bp_}_p{p_}": fusion_compare(bp_, p_, K, local)
+                                       for bp_, p_ in ((3, 7), (5, 7), (3, 4))}
     print(json.dumps(line), flush=True)
 
 
@@ -403,6 +407,61 @@ def p_sweep(bp: int, K: int, local: int, ps=(2, 3, 4, 5, 6, 8), dofs: float = 50
             torch.cuda.empty_cache()
         except Exception as ex:
             out[str(p)] = {"error": str(ex)[:120]}
+    return out
+
+
+def fusion_compare(bp: int, p: int, K: int, local: int, dofs: float = 30_000_000):
+    """ms per constrained operator apply and per CG iteration on one mesh,
+    fused kernel (fast and reference arithmetic) vs the multipass backend
+    (always reference arithmetic), CUDA events on the launching stream."""
+    import torch
+
+    import paper_2109_05072_b200 as hx
+
+    e = 1
+    while ((e + 1) * p + 1) ** 3 <= dofs:
+        e += 1
+    dims = (e, e, e)
+    out = {"dims": list(dims)}
+    try:
+        setup = hx.make_setup(hx.BPKind(bp), hx.build_box_mesh(dims, p), device=local)
+        b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda(local)
+        u = torch.rand_like(b)
+        w = torch.empty_like(b)
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        for name, backend, mode in (("fused_fast", hx.Backend.Cuda, "fast"),
+                                    ("fused_reference", hx.Backend.Cuda, "reference"),
+                                    ("multipass", hx.Backend.CudaMultipass, "reference")):
+            op = hx.OperatorHandle(backend, setup)
+            op.workspace().set_mode(mode)
+            A = hx.ConstrainedOperator(op) if bp != 1 else op
+            for _ in range(3):
+                A.apply(u, w)
+            torch.cuda.synchronize()
+            ea, eb = ev(), ev()
+            ea.record()
+            for _ in range(K):
+                A.apply(u, w)
+            eb.record()
+            torch.cuda.synchronize()
+            t_apply = ea.elapsed_time(eb) / K
+            x = torch.zeros_like(b)
+            hx.cg(A, b, x, 0.0, 3, mode=mode)
+            x.zero_()
+            torch.cuda.synchronize()
+            ea.record()
+            hx.cg(A, b, x, 0.0, K, mode=mode)
+            eb.record()
+            torch.cuda.synchronize()
+            t_it = ea.elapsed_time(eb) / K
+            out[name] = {"ms_per_apply": t_apply, "ms_per_cg_iter": t_it, "cg_GDOFps": b.numel() / t_it / 1e6}
+            del op, A, x
+            torch.cuda.empty_cache()
+        out["apply_speedup_fused_fast_vs_multipass"] = out["multipass"]["ms_per_apply"] / out["fused_fast"]["ms_per_apply"]
+        del setup, b, u, w
+        torch.cuda.empty_cache()
+    except Exception as ex:
+        out["error"] = str(ex)[:160]
     return out
 
 

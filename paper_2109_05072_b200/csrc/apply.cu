@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "device_util.cuh"
@@ -97,53 +98,140 @@ struct alignas(16) BasisT {  // 16-byte aligned kernel parameter: paired constan
   double D[Q][P + 1];
 };
 
-template <int P, int Q, int KIND>
+// Work split of the element kernel, per (P, KIND), as a code
+// SK = R*100 + S*10 + KC: S lanes share each pencil (lane s owns quadrature
+// rows s, s+S, ...; the transposed contractions' partial sums are
+// reduce-scattered by warp shuffles), KC element columns share a CTA, and
+// R*8 caps the registers (R = 0: 255). S divides the 2 Q (P+1) basis
+// coefficients a thread keeps in registers; KC fills the warps when Q^2 is
+// small. Values: measured per p on a B200 (profiles/README.md).
+constexpr int sk_default(int kind, int p) {
+  // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
+  constexpr int mass[9] = {0, 18, 16, 16, 14, 13, 11, 11, 1611};
+  constexpr int diff[9] = {0, 17, 12, 13, 1812, 2111, 11, 11, 11};
+  constexpr int coll[9] = {0, 18, 13, 12, 12, 12, 12, 11, 11};
+  return kind == 0 ? mass[p] : kind == 1 ? diff[p] : coll[p];
+}
+// Candidate codes compiled for (KIND, P); the first is the default. A sweep
+// build (-DHX_SK_SWEEP='"header"', tools/build_variant.py) specialises this
+// with more candidates, selected at run time by HEXBP_SK_<kind>_<p>=<code>.
+template <int KIND, int P>
+struct SkList {
+  static constexpr int n = 1;
+  static constexpr int v[1] = {sk_default(KIND, P)};
+};
+#ifdef HX_SK_SWEEP
+#include HX_SK_SWEEP
+#endif
+
+template <int P, int Q, int KIND, int SK>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int QQ = Q * Q;
-  static constexpr int NT = ((QQ + 31) / 32) * 32;
+  static constexpr int S = SK / 10 % 10;  // lanes per pencil (1, 2, 4)
+  static constexpr int KC = SK % 10;      // element columns per CTA
+  static constexpr int MAXREG = SK / 100 ? SK / 100 * 8 : 255;
+  static constexpr int RQ = (Q + S - 1) / S;      // quadrature rows per lane
+  static constexpr int RN = (N + S - 1) / S;      // node outputs per lane (transposed phases)
+  static constexpr int ZI = KC * N * N, YI = KC * N * Q, XI = KC * QQ;  // pencils per phase
+  static constexpr int NT = ((S * XI + 31) / 32) * 32;
   static constexpr int FA = KIND == KIND_MASS ? 1 : 2;  // fields in smem A ([f][c][j][i])
   static constexpr int FB = KIND == KIND_MASS ? 1 : 3;  // fields in smem B ([f][i][c][b])
   static constexpr int SA_CS = best_stride(N, Q, N * N, 0);
   static constexpr int SB_IS = best_stride(N, Q, Q * Q, 1);
   static constexpr int SA_SIZE = FA * Q * SA_CS;
   static constexpr int SB_SIZE = FB * N * SB_IS;
+  static constexpr int CB = (SA_SIZE + SB_SIZE + 1) / 2 * 2;  // per-column scratch (A then B)
   static constexpr int COMP = KIND == KIND_MASS ? 1 : 6;
   static constexpr int GS = (COMP * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
-  static constexpr int G_OFF = (SA_SIZE + SB_SIZE + 1) / 2 * 2;  // 16-byte aligned TMA destination
-  static constexpr int U_OFF = G_OFF + GS;                       // two u slabs (cp.async double buffer)
-  static constexpr int BAR_OFF = U_OFF + 2 * N * N * N;
+  static constexpr int G_OFF = KC * CB;                      // 16-byte aligned TMA destinations
+  static constexpr int U_OFF = G_OFF + KC * GS;              // per column two u slabs (cp.async double buffer)
+  static constexpr int BAR_OFF = U_OFF + KC * 2 * N * N * N;
   static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
-  // ptxas sizes the register cap as if CTAs were whole 4-warp groups; these
-  // values leave the cap at 255 and let registers/smem set the occupancy.
-  // (P = 4 stiffness: ptxas spills uniform registers into vector registers
-  // (R2UR per basis coefficient) and reaches 194 registers unless capped; six
-  // CTAs per SM measured faster despite a small spill.)
-  static constexpr int MIN_BLOCKS =
-      NT <= 32 ? 8 : (NT <= 64 ? (P == 4 && KIND != KIND_MASS ? 6 : 4) : (NT <= 96 ? 3 : 2));
 };
 
-template <int P, int Q, int KIND>
-__global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOCKS)
+// a[S r + s] for compile-time r and the lane's runtime s (0 past the end)
+template <int S, int L>
+__device__ __forceinline__ double pick(const double (&a)[L], int r, int s) {
+  double v = 0.0;
+#pragma unroll
+  for (int q = 0; q < S; ++q)
+    if (S * r + q < L && s == q) v = a[S * r + q];
+  return v;
+}
+
+// Reduce-scatter over the S lanes of a pencil: lane s receives
+// o[r] = sum over the group's lanes of v[S r + s]. Two-term sums are
+// commutative, so every lane of a pair forms the identical value.
+template <int S, int L, int R>
+__device__ __forceinline__ void reduce_scatter(const double (&v)[L], double (&o)[R], int s) {
+  auto at = [&](int j) -> double { return j < L ? v[j] : 0.0; };
+  if constexpr (S == 1) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) o[r] = at(r);
+  } else if constexpr (S == 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double v0 = at(2 * r), v1 = at(2 * r + 1);
+      const double mine = s ? v1 : v0, send = s ? v0 : v1;
+      o[r] = mine + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+  } else {
+    static_assert(S == 4, "S in {1, 2, 4}");
+    const int b1 = (s >> 1) & 1, b0 = s & 1;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double w[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double lo = at(4 * r + e), hi = at(4 * r + 2 + e);
+        w[e] = (b1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
+      }
+      o[r] = (b0 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, b0 ? w[0] : w[1], 1);
+    }
+  }
+}
+
+template <int P, int Q, int KIND, int SK, typename K_ = Cfg<P, Q, KIND, SK>>
+__global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs) {
-  using K = Cfg<P, Q, KIND>;
-  constexpr int N = K::N, QQ = K::QQ, NT = K::NT;
+  using K = Cfg<P, Q, KIND, SK>;
+  constexpr int N = K::N, QQ = K::QQ, NT = K::NT, S = K::S, KC = K::KC, RQ = K::RQ, RN = K::RN;
   constexpr bool COLLOC = KIND == KIND_COLLOC;
   constexpr bool MASS = KIND == KIND_MASS;
 
   extern __shared__ double smem[];
-  double* SA = smem;
-  double* SB = smem + K::SA_SIZE;
   __shared__ double s_red[NT / 32];
 
   if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;  // CG already stopped
 
   const int t = threadIdx.x;
+  const int s = t % S;     // lane within the pencil group
+  const int item = t / S;  // pencil index (per phase)
+  const int wfirst = (t & ~31) / S;  // first pencil of this warp: whole-warp phase skips
   const uint64_t pol = policy_evict_first();
   const bool do_dot = A.col_dot != nullptr;
-  const bool zrole = t < N * N;
-  const int zi = t % N, zj = t / N;
-  const int col = blockIdx.x;
+  const int col0 = blockIdx.x * KC;
+  const int kv = A.ncols - col0 < KC ? A.ncols - col0 : KC;  // valid columns of this CTA
+
+  // basis rows of this lane: cB[r][i] = B(S r + s, i), cD likewise (0 past Q)
+  double cB[RQ][N], cD[RQ][N];
+#pragma unroll
+  for (int r = 0; r < RQ; ++r)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int c = S * r + (S == 1 ? 0 : s);
+      cB[r][i] = c < Q ? bs.B[c][i] : 0.0;
+      cD[r][i] = c < Q ? bs.D[c][i] : 0.0;
+    }
+
+  // z-pencil role: pencil (zi, zj) of column kz
+  const bool zrole = item < K::ZI;
+  const int zit = zrole ? item : K::ZI - 1;
+  const int kz = zit / (N * N), pz = zit % (N * N);
+  const int zi = pz % N, zj = pz / N;
+  const int col = col0 + kz;
+  const bool zvalid = zrole && kz < kv;
   const int ex = col % A.nx, ey = col / A.nx;
   const int X = ex * P + zi, Y = ey * P + zj;
   const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
@@ -151,40 +239,46 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
   const bool owner = ring_owner(P, zi, zj, ex, ey, A.nx, A.ny);
   const LatLayout L(P, A.nx, A.ny);
   bool lat_is_y = false;
-  const long long lat0 = ring ? lat_store_index(L, P, A.nx, ex, ey, zi, zj, 0, lat_is_y) : 0;
+  const long long lat0 = (ring && zvalid) ? lat_store_index(L, P, A.nx, ex, ey, zi, zj, 0, lat_is_y) : 0;
   double* lat = (lat_is_y ? A.lateral : A.lat_x) + lat0;
   const long long lat_stride = lat_is_y ? L.y_zstride : L.x_zstride;
   double carry = 0.0, dot = 0.0;
 
-  // Staging: the element's factor block G_e is copied global -> shared by the
+  // Staging: each column's factor block G_e is copied global -> shared by the
   // TMA bulk engine (one elected thread, mbarrier completion), issued as soon
-  // as the previous element's phase X has consumed the buffer; the z-pencil of
-  // u for element ez+1 is fetched by LDGSTS (cp.async) into the other half of a
-  // double buffer while element ez computes. Neither costs registers.
-  const double* Gcol = A.G + static_cast<long long>(col) * A.nz * K::GS;
+  // as the previous element's phase X has consumed the buffer; the z-pencils
+  // of u for element ez+1 are fetched by LDGSTS (cp.async) into the other half
+  // of a double buffer while element ez computes. Neither costs registers.
   constexpr uint32_t gbytes = K::GS * 8;
-  double* Gs = smem + K::G_OFF;
-  double* Us = smem + K::U_OFF;
   const uint32_t bar = smem_u32(smem + K::BAR_OFF);
-  const uint32_t gs_addr = smem_u32(Gs);
+  const long long gcol = static_cast<long long>(A.nz) * K::GS;  // doubles per column of G
+  const double* Gcta = A.G + static_cast<long long>(col0) * gcol;
   if (t == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
+  auto issue_g = [&](int ez) {  // thread 0
+    mbar_arrive_expect_tx(bar, gbytes * kv);
+    for (int kk = 0; kk < kv; ++kk)
+      bulk_g2s(smem_u32(smem + K::G_OFF + kk * K::GS), Gcta + kk * gcol + ez * K::GS, gbytes, bar, pol);
+  };
   if (t == 0) {
-    mbar_arrive_expect_tx(bar, gbytes);
-    bulk_g2s(gs_addr, Gcol, gbytes, bar, pol);
-    if (A.nz > 1) prefetch_l2_bulk(Gcol + K::GS, gbytes);
+    issue_g(0);
+    if (A.nz > 1)
+      for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + K::GS, gbytes);
   }
+  double* Uz = smem + K::U_OFF + kz * 2 * N * N * N + pz;  // this z-pencil's u staging (buffer 0)
   auto fetch_u = [&](int ez, int buf) {
-    if (zrole) {
-      const uint32_t dst = smem_u32(Us + buf * N * N * N + t);
+    if (zvalid) {
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const long long node =
-            X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * (ez * P + k));
-        cp_async8(dst + k * N * N * 8, A.u + node);
+      for (int r = 0; r < RN; ++r) {
+        const int k = S * r + s;
+        if (k < N) {
+          const long long node =
+              X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * (ez * P + k));
+          cp_async8(smem_u32(Uz + buf * N * N * N + k * N * N), A.u + node);
+        }
       }
     }
     cp_async_commit();
@@ -192,20 +286,21 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
   fetch_u(0, 0);
 
   for (int ez = 0; ez < A.nz; ++ez) {
-    if (t == 0 && ez + 2 < A.nz) prefetch_l2_bulk(Gcol + (ez + 2) * K::GS, gbytes);
-    const double* Ge = Gs;
-    double out[N];
+    if (t == 0 && ez + 2 < A.nz)
+      for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + (ez + 2) * K::GS, gbytes);
     if (ez + 1 < A.nz) {
       fetch_u(ez + 1, (ez + 1) & 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
+    if constexpr (S > 1) __syncthreads();  // the lanes of a pencil fetched its nodes in turn
 
     // ---------------- phase Z: gather the z-pencil, contract along z
-    if (zrole) {
+    if (wfirst < K::ZI) {
+      double* SA = smem + kz * K::CB;
       double uk[N];
-      const double* us = Us + (ez & 1) * N * N * N + t;
+      const double* us = Uz + (ez & 1) * N * N * N;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         const int Z = ez * P + k;
@@ -214,29 +309,36 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
         uk[k] = v;
       }
 #pragma unroll
-      for (int c = 0; c < Q; ++c) {
-        double s0;
+      for (int r = 0; r < RQ; ++r) {
+        const int c = S * r + s;
+        double s0, s1 = 0.0;
         if constexpr (COLLOC) {
-          s0 = uk[c];
+          s0 = pick<S>(uk, r, s);
         } else {
           s0 = 0.0;
 #pragma unroll
-          for (int k = 0; k < N; ++k) s0 = fma(bs.B[c][k], uk[k], s0);
+          for (int k = 0; k < N; ++k) s0 = fma(cB[r][k], uk[k], s0);
         }
-        SA[c * K::SA_CS + t] = s0;
         if constexpr (!MASS) {
-          double s1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < N; ++k) s1 = fma(bs.D[c][k], uk[k], s1);
-          SA[(Q + c) * K::SA_CS + t] = s1;
+          for (int k = 0; k < N; ++k) s1 = fma(cD[r][k], uk[k], s1);
+        }
+        if (zrole && c < Q) {
+          SA[c * K::SA_CS + pz] = s0;
+          if constexpr (!MASS) SA[(Q + c) * K::SA_CS + pz] = s1;
         }
       }
     }
     __syncthreads();
 
     // ---------------- phase Y: y-pencils
-    if (t < N * Q) {
-      const int i = t % N, c = t / N;
+    if (wfirst < K::YI) {
+      const bool act = item < K::YI;
+      const int it = act ? item : K::YI - 1;
+      const int ky = it / (N * Q), rem = it % (N * Q);
+      const int i = rem % N, c = rem / N;
+      const double* SA = smem + ky * K::CB;
+      double* SB = smem + ky * K::CB + K::SA_SIZE;
       double y0[N], y1[N];
 #pragma unroll
       for (int j = 0; j < N; ++j) {
@@ -245,231 +347,284 @@ __global__ void __launch_bounds__(Cfg<P, Q, KIND>::NT, Cfg<P, Q, KIND>::MIN_BLOC
       }
       double* sb = SB + i * K::SB_IS + c * Q;
 #pragma unroll
-      for (int b = 0; b < Q; ++b) {
+      for (int r = 0; r < RQ; ++r) {
+        const int b = S * r + s;
         double bb = 0.0, db = 0.0, bd = 0.0;
         if constexpr (COLLOC) {
-          bb = y0[b];
-          bd = y1[b];
+          bb = pick<S>(y0, r, s);
+          bd = pick<S>(y1, r, s);
         } else {
 #pragma unroll
-          for (int j = 0; j < N; ++j) bb = fma(bs.B[b][j], y0[j], bb);
+          for (int j = 0; j < N; ++j) bb = fma(cB[r][j], y0[j], bb);
           if constexpr (!MASS) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) bd = fma(bs.B[b][j], y1[j], bd);
+            for (int j = 0; j < N; ++j) bd = fma(cB[r][j], y1[j], bd);
           }
         }
-        sb[b] = bb;
         if constexpr (!MASS) {
 #pragma unroll
-          for (int j = 0; j < N; ++j) db = fma(bs.D[b][j], y0[j], db);
-          sb[N * K::SB_IS + b] = db;
-          sb[2 * N * K::SB_IS + b] = bd;
+          for (int j = 0; j < N; ++j) db = fma(cD[r][j], y0[j], db);
+        }
+        if (act && b < Q) {
+          sb[b] = bb;
+          if constexpr (!MASS) {
+            sb[N * K::SB_IS + b] = db;
+            sb[2 * N * K::SB_IS + b] = bd;
+          }
         }
       }
     }
     __syncthreads();
 
     // ---------------- phase X: x-pencils, pointwise factors, back along x
-    mbar_wait_parity(bar, ez & 1);  // G_e has landed in shared memory
-    if (t < QQ) {
+    mbar_wait_parity(bar, ez & 1);  // the G blocks have landed in shared memory
+    if (wfirst < K::XI) {
+      const bool act = item < K::XI;
+      const int it = act ? item : K::XI - 1;
+      const int kx = it / QQ, pp = it % QQ;
+      double* SB = smem + kx * K::CB + K::SA_SIZE;
+      const double* Ge = smem + K::G_OFF + kx * K::GS;
       if constexpr (MASS) {
-        double x0[N], v[Q];
+        double x0[N], v[RQ];
 #pragma unroll
-        for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + t];
+        for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + pp];
 #pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double s = 0.0;
+        for (int r = 0; r < RQ; ++r) {
+          const int a = S * r + s;
+          double acc = 0.0;
 #pragma unroll
-          for (int i = 0; i < N; ++i) s = fma(bs.B[a][i], x0[i], s);
-          v[a] = s * Ge[a * QQ + t];
+          for (int i = 0; i < N; ++i) acc = fma(cB[r][i], x0[i], acc);
+          v[r] = a < Q ? acc * Ge[a * QQ + pp] : 0.0;
         }
+        double part[N], o[RN];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          double s = 0.0;
+          double acc = 0.0;
 #pragma unroll
-          for (int a = 0; a < Q; ++a) s = fma(bs.B[a][i], v[a], s);
-          SB[i * K::SB_IS + t] = s;
+          for (int r = 0; r < RQ; ++r) acc = fma(cB[r][i], v[r], acc);
+          part[i] = acc;
         }
+        reduce_scatter<S>(part, o, s);
+#pragma unroll
+        for (int r = 0; r < RN; ++r)
+          if (act && S * r + s < N) SB[(S * r + s) * K::SB_IS + pp] = o[r];
       } else {
-        double gr[Q], gs[Q], gt[Q];
+        double gr[RQ], gs[RQ], gt[RQ];
         {
           double x0[N], x1[N], x2[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            x0[i] = SB[i * K::SB_IS + t];
-            x1[i] = SB[(N + i) * K::SB_IS + t];
-            x2[i] = SB[(2 * N + i) * K::SB_IS + t];
+            x0[i] = SB[i * K::SB_IS + pp];
+            x1[i] = SB[(N + i) * K::SB_IS + pp];
+            x2[i] = SB[(2 * N + i) * K::SB_IS + pp];
           }
 #pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            double r = 0.0;
+          for (int r = 0; r < RQ; ++r) {
+            double rr = 0.0;
 #pragma unroll
-            for (int i = 0; i < N; ++i) r = fma(bs.D[a][i], x0[i], r);
-            gr[a] = r;
+            for (int i = 0; i < N; ++i) rr = fma(cD[r][i], x0[i], rr);
+            gr[r] = rr;
             if constexpr (COLLOC) {
-              gs[a] = x1[a];
-              gt[a] = x2[a];
+              gs[r] = pick<S>(x1, r, s);
+              gt[r] = pick<S>(x2, r, s);
             } else {
-              double s = 0.0, u = 0.0;
+              double ss = 0.0, uu = 0.0;
 #pragma unroll
               for (int i = 0; i < N; ++i) {
-                s = fma(bs.B[a][i], x1[i], s);
-                u = fma(bs.B[a][i], x2[i], u);
+                ss = fma(cB[r][i], x1[i], ss);
+                uu = fma(cB[r][i], x2[i], uu);
               }
-              gs[a] = s;
-              gt[a] = u;
+              gs[r] = ss;
+              gt[r] = uu;
             }
           }
         }
 #pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          const double* g = Ge + a * QQ + t;
+        for (int r = 0; r < RQ; ++r) {
+          const int a = S * r + s;
+          const int ac = a < Q ? a : Q - 1;
+          const double* g = Ge + ac * QQ + pp;
           const double g0 = g[0 * Q * QQ], g1 = g[1 * Q * QQ], g2 = g[2 * Q * QQ];
           const double g3 = g[3 * Q * QQ], g4 = g[4 * Q * QQ], g5 = g[5 * Q * QQ];
-          const double r = gr[a], s = gs[a], u = gt[a];
-          gr[a] = g0 * r + g1 * s + g2 * u;  // operator.hpp:129-131
-          gs[a] = g1 * r + g3 * s + g4 * u;
-          gt[a] = g2 * r + g4 * s + g5 * u;
+          const double rr = gr[r], ss = gs[r], uu = gt[r];
+          const bool ok = S == 1 || a < Q;
+          gr[r] = ok ? g0 * rr + g1 * ss + g2 * uu : 0.0;  // operator.hpp:129-131
+          gs[r] = ok ? g1 * rr + g3 * ss + g4 * uu : 0.0;
+          gt[r] = ok ? g2 * rr + g4 * ss + g5 * uu : 0.0;
         }
+        // back along x, field by field (partials reduce-scattered over the pencil's lanes)
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int f = 0; f < 3; ++f) {
+          double part[N], o[RN];
 #pragma unroll
-          for (int a = 0; a < Q; ++a) a1 = fma(bs.D[a][i], gr[a], a1);
-          if constexpr (COLLOC) {
-            a2 = gs[i];
-            a3 = gt[i];
-          } else {
+          for (int i = 0; i < N; ++i) {
+            double acc = 0.0;
+            if (f == 0) {
 #pragma unroll
-            for (int a = 0; a < Q; ++a) {
-              a2 = fma(bs.B[a][i], gs[a], a2);
-              a3 = fma(bs.B[a][i], gt[a], a3);
+              for (int r = 0; r < RQ; ++r) acc = fma(cD[r][i], gr[r], acc);
+            } else if constexpr (COLLOC) {
+              acc = (S == 1 || s == i % S) ? (f == 1 ? gs[i / S] : gt[i / S]) : 0.0;
+            } else {
+#pragma unroll
+              for (int r = 0; r < RQ; ++r) acc = fma(cB[r][i], f == 1 ? gs[r] : gt[r], acc);
             }
+            part[i] = acc;
           }
-          SB[i * K::SB_IS + t] = a1;
-          SB[(N + i) * K::SB_IS + t] = a2;
-          SB[(2 * N + i) * K::SB_IS + t] = a3;
+          reduce_scatter<S>(part, o, s);
+#pragma unroll
+          for (int r = 0; r < RN; ++r)
+            if (act && S * r + s < N) SB[(f * N + S * r + s) * K::SB_IS + pp] = o[r];
         }
       }
     }
     __syncthreads();
-    if (t == 0 && ez + 1 < A.nz) {  // G buffer consumed: stream the next element's block
+    if (t == 0 && ez + 1 < A.nz) {  // G buffers consumed: stream the next element's blocks
       fence_proxy_async();
-      mbar_arrive_expect_tx(bar, gbytes);
-      bulk_g2s(gs_addr, Gcol + (ez + 1) * K::GS, gbytes, bar, pol);
+      issue_g(ez + 1);
     }
 
     // ---------------- phase Y': back along y
-    if (t < N * Q) {
-      const int i = t % N, c = t / N;
-      const double* sb = SB + i * K::SB_IS + c * Q;
-      double a0[Q], a1[Q], a2[Q];
+    if (wfirst < K::YI) {
+      const bool act = item < K::YI;
+      const int it = act ? item : K::YI - 1;
+      const int ky = it / (N * Q), rem = it % (N * Q);
+      const int i = rem % N, c = rem / N;
+      double* SA = smem + ky * K::CB;
+      const double* sb = smem + ky * K::CB + K::SA_SIZE + i * K::SB_IS + c * Q;
+      double a0[RQ], a1[RQ], a2[RQ];
 #pragma unroll
-      for (int b = 0; b < Q; ++b) {
-        a0[b] = sb[b];
+      for (int r = 0; r < RQ; ++r) {
+        const int b = S * r + s;
+        const int bc = b < Q ? b : Q - 1;  // past-the-end rows carry zero coefficients
+        a0[r] = sb[bc];
         if constexpr (!MASS) {
-          a1[b] = sb[N * K::SB_IS + b];
-          a2[b] = sb[2 * N * K::SB_IS + b];
+          a1[r] = sb[N * K::SB_IS + bc];
+          a2[r] = sb[2 * N * K::SB_IS + bc];
         }
       }
+      double p1[N], p2[N], o1[RN], o2[RN];
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double c1 = 0.0, c2 = 0.0;
+        const bool mine = S == 1 || s == j % S;
         if constexpr (MASS) {
 #pragma unroll
-          for (int b = 0; b < Q; ++b) c1 = fma(bs.B[b][j], a0[b], c1);
+          for (int r = 0; r < RQ; ++r) c1 = fma(cB[r][j], a0[r], c1);
         } else if constexpr (COLLOC) {
-          c1 = a0[j];
+          c1 = mine ? a0[j / S] : 0.0;
 #pragma unroll
-          for (int b = 0; b < Q; ++b) c1 = fma(bs.D[b][j], a1[b], c1);
-          c2 = a2[j];
+          for (int r = 0; r < RQ; ++r) c1 = fma(cD[r][j], a1[r], c1);
+          c2 = mine ? a2[j / S] : 0.0;
         } else {
 #pragma unroll
-          for (int b = 0; b < Q; ++b) {
-            c1 = fma(bs.B[b][j], a0[b], c1);
-            c2 = fma(bs.B[b][j], a2[b], c2);
+          for (int r = 0; r < RQ; ++r) {
+            c1 = fma(cB[r][j], a0[r], c1);
+            c2 = fma(cB[r][j], a2[r], c2);
           }
 #pragma unroll
-          for (int b = 0; b < Q; ++b) c1 = fma(bs.D[b][j], a1[b], c1);
+          for (int r = 0; r < RQ; ++r) c1 = fma(cD[r][j], a1[r], c1);
         }
-        SA[c * K::SA_CS + j * N + i] = c1;
-        if constexpr (!MASS) SA[(Q + c) * K::SA_CS + j * N + i] = c2;
+        p1[j] = c1;
+        p2[j] = c2;
+      }
+      reduce_scatter<S>(p1, o1, s);
+      if constexpr (!MASS) reduce_scatter<S>(p2, o2, s);
+#pragma unroll
+      for (int r = 0; r < RN; ++r) {
+        const int j = S * r + s;
+        if (act && j < N) {
+          SA[c * K::SA_CS + j * N + i] = o1[r];
+          if constexpr (!MASS) SA[(Q + c) * K::SA_CS + j * N + i] = o2[r];
+        }
       }
     }
     __syncthreads();
 
     // ---------------- phase Z': back along z into the z-pencil
-    if (zrole) {
-      double c1[Q], c2[Q];
+    if (wfirst < K::ZI) {
+      const double* SA = smem + kz * K::CB;
+      double c1[RQ], c2[RQ];
 #pragma unroll
-      for (int c = 0; c < Q; ++c) {
-        c1[c] = SA[c * K::SA_CS + t];
-        if constexpr (!MASS) c2[c] = SA[(Q + c) * K::SA_CS + t];
+      for (int r = 0; r < RQ; ++r) {
+        const int c = S * r + s;
+        const int cc = c < Q ? c : Q - 1;
+        c1[r] = SA[cc * K::SA_CS + pz];
+        if constexpr (!MASS) c2[r] = SA[(Q + cc) * K::SA_CS + pz];
       }
+      double part[N], out[RN];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        double s = 0.0;
+        double acc = 0.0;
         if constexpr (COLLOC) {
-          s = c1[k];
+          acc = (S == 1 || s == k % S) ? c1[k / S] : 0.0;
         } else {
 #pragma unroll
-          for (int c = 0; c < Q; ++c) s = fma(bs.B[c][k], c1[c], s);
+          for (int r = 0; r < RQ; ++r) acc = fma(cB[r][k], c1[r], acc);
         }
         if constexpr (!MASS) {
 #pragma unroll
-          for (int c = 0; c < Q; ++c) s = fma(bs.D[c][k], c2[c], s);
+          for (int r = 0; r < RQ; ++r) acc = fma(cD[r][k], c2[r], acc);
         }
-        out[k] = s;
+        part[k] = acc;
       }
+      reduce_scatter<S>(part, out, s);
 
       // ---------------- transpose restriction, part 1 (see header)
-      out[0] += carry;
+      if (s == 0) out[0] += carry;  // node k = 0 belongs to lane 0
+      // the top plane's value is the next element's carry (lane P % S -> lane 0)
+      const double top = out[P / S];
+      carry = S == 1 ? top : __shfl_sync(0xffffffffu, top, (t & 31) - s + P % S);
       const int kend = (ez == A.nz - 1) ? N : P;
-      const double* usz = Us + (ez & 1) * N * N * N + t;  // u of this element, still staged
-      if (!do_dot) {  // plain apply: the lean epilogue (keeps ptxas' uniform registers for the basis)
+      const double* usz = Uz + (ez & 1) * N * N * N;  // u of this element, still staged
+      if (zvalid) {
+        if (!do_dot) {  // plain apply: the lean epilogue
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          if (k < kend) {
-            const int Z = ez * P + k;
-            if (ring) {
-              lat[Z * lat_stride] = out[k];
-            } else {
-              const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-              double v = out[k];
-              if (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = usz[k * N * N];
-              A.w[node] = v;
+          for (int r = 0; r < RN; ++r) {
+            const int k = S * r + s;
+            if (k < kend) {
+              const int Z = ez * P + k;
+              if (ring) {
+                lat[Z * lat_stride] = out[r];
+              } else {
+                const long long node =
+                    X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+                double v = out[r];
+                if (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = usz[k * N * N];
+                A.w[node] = v;
+              }
             }
           }
-        }
-      } else {
+        } else {
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          if (k < kend) {
-            const int Z = ez * P + k;
-            const double uv = usz[k * N * N];
-            const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
-            if (ring) {
-              lat[Z * lat_stride] = out[k];
-              // column-local share of p.Ap on the ring (ring.cuh); w = u rows counted once
-              if (bcxy || zbc)
-                dot = owner ? fma(uv, uv, dot) : dot;
-              else
-                dot = fma(uv, out[k], dot);
-            } else {
-              const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-              const double v = zbc ? uv : out[k];
-              A.w[node] = v;
-              dot = fma(uv, v, dot);
+          for (int r = 0; r < RN; ++r) {
+            const int k = S * r + s;
+            if (k < kend) {
+              const int Z = ez * P + k;
+              const double uv = usz[k * N * N];
+              const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+              if (ring) {
+                lat[Z * lat_stride] = out[r];
+                // column-local share of p.Ap on the ring (ring.cuh); w = u rows counted once
+                if (bcxy || zbc)
+                  dot = owner ? fma(uv, uv, dot) : dot;
+                else
+                  dot = fma(uv, out[r], dot);
+              } else {
+                const long long node =
+                    X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+                const double v = zbc ? uv : out[r];
+                A.w[node] = v;
+                dot = fma(uv, v, dot);
+              }
             }
           }
         }
       }
-      carry = out[P];
     }
-    __syncthreads();  // smem A is rewritten by the next element's phase Z
+    __syncthreads();  // smem A and the u buffer are rewritten next element
   }
   const double cdot = do_dot ? block_sum<NT>(dot, s_red) : 0.0;
-  ring_dot_finish<NT>(A, col, cdot, s_red);
+  ring_dot_finish<NT>(A, blockIdx.x, cdot, s_red);
 }
 
 // Transpose restriction, part 2, for plain applies: every ring node sums its
@@ -502,21 +657,64 @@ __global__ void __launch_bounds__(FT) lateral_fixup_kernel(const __grid_constant
   }
 }
 
-template <int P, int Q, int KIND>
+template <int P, int Q, int KIND, int SK>
 void* kernel_ptr() {
   static bool configured = false;  // opt in to > 48 KB dynamic shared memory once per instantiation
   if (!configured) {
-    cudaFuncSetAttribute(&bp_apply_kernel<P, Q, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<P, Q, KIND>::SMEM_BYTES);
+    cudaFuncSetAttribute(&bp_apply_kernel<P, Q, KIND, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<P, Q, KIND, SK>::SMEM_BYTES);
     configured = true;
   }
-  return reinterpret_cast<void*>(&bp_apply_kernel<P, Q, KIND>);
+  return reinterpret_cast<void*>(&bp_apply_kernel<P, Q, KIND, SK>);
 }
 
-template <int P, int Q, int KIND>
+// the SK code in use for (kind, p): the default, or HEXBP_SK_<kind>_<p> when
+// a sweep build compiled that candidate
+int sk_select(int kind, int p, int dflt) {
+  static int cache[3][9] = {};
+  int& c = cache[kind][p];
+#ifdef HX_SK_SWEEP
+  c = 0;  // sweep builds re-read the environment at every launch
+#endif
+  if (c == 0) {
+    c = dflt;
+    char name[32];
+    std::snprintf(name, sizeof(name), "HEXBP_SK_%d_%d", kind, p);
+    if (const char* v = std::getenv(name)) c = std::atoi(v);
+  }
+  return c;
+}
+
+struct KInfo {
+  void* fn;
+  int nt;
+  int smem;
+  int cols;  // element columns per CTA
+};
+
+template <int P, int Q, int KIND, int I = 0>
+KInfo info_sel(int sk) {
+  using L = SkList<KIND, P>;
+  if constexpr (I < L::n) {
+    constexpr int c = L::v[I];
+    using K = Cfg<P, Q, KIND, c>;
+    if (sk == c) return {kernel_ptr<P, Q, KIND, c>(), K::NT, K::SMEM_BYTES, K::KC};
+    return info_sel<P, Q, KIND, I + 1>(sk);
+  } else {
+    return {nullptr, 0, 0, 1};
+  }
+}
+
+template <int P, int KIND>
+KInfo info_t() {
+  constexpr int Q = KIND == KIND_COLLOC ? P + 1 : P + 2;
+  return info_sel<P, Q, KIND>(sk_select(KIND, P, SkList<KIND, P>::v[0]));
+}
+
+template <int P, int Q, int KIND, int SK>
 cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  using K = Cfg<P, Q, KIND>;
-  kernel_ptr<P, Q, KIND>();
+  using K = Cfg<P, Q, KIND, SK>;
+  kernel_ptr<P, Q, KIND, SK>();
   if (s.gstride != K::GS) return cudaErrorInvalidValue;
   BasisT<P, Q> bs;
   for (int i = 0; i < Q; ++i)
@@ -524,21 +722,19 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
       bs.B[i][j] = s.B[i * (P + 1) + j];
       bs.D[i][j] = s.D[i * (P + 1) + j];
     }
-  bp_apply_kernel<P, Q, KIND><<<a.ncols, K::NT, K::SMEM_BYTES, st>>>(a, bs);
+  bp_apply_kernel<P, Q, KIND, SK><<<(a.ncols + K::KC - 1) / K::KC, K::NT, K::SMEM_BYTES, st>>>(a, bs);
   return cudaGetLastError();
 }
 
-struct KInfo {
-  void* fn;
-  int nt;
-  int smem;
-};
-
-template <int P, int KIND>
-KInfo info_t() {
-  constexpr int Q = KIND == KIND_COLLOC ? P + 1 : P + 2;
-  using K = Cfg<P, Q, KIND>;
-  return {kernel_ptr<P, Q, KIND>(), K::NT, K::SMEM_BYTES};
+template <int P, int Q, int KIND, int I = 0>
+cudaError_t launch_sel(int sk, const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  using L = SkList<KIND, P>;
+  if constexpr (I < L::n) {
+    if (sk == L::v[I]) return launch_t<P, Q, KIND, L::v[I]>(s, a, st);
+    return launch_sel<P, Q, KIND, I + 1>(sk, s, a, st);
+  } else {
+    return cudaErrorInvalidValue;  // code not compiled in
+  }
 }
 
 template <int KIND>
@@ -553,7 +749,7 @@ KInfo info_k(int p) {
     case 7: return info_t<7, KIND>();
     case 8: return info_t<8, KIND>();
   }
-  return {nullptr, 0, 0};
+  return {nullptr, 0, 0, 1};
 }
 
 KInfo info_for(const Setup& s) {
@@ -562,21 +758,26 @@ KInfo info_for(const Setup& s) {
     case KIND_DIFF: return info_k<KIND_DIFF>(s.p);
     case KIND_COLLOC: return info_k<KIND_COLLOC>(s.p);
   }
-  return {nullptr, 0, 0};
+  return {nullptr, 0, 0, 1};
+}
+
+template <int P, int KIND>
+cudaError_t launch_p(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  constexpr int Q = KIND == KIND_COLLOC ? P + 1 : P + 2;
+  return launch_sel<P, Q, KIND>(sk_select(KIND, P, SkList<KIND, P>::v[0]), s, a, st);
 }
 
 template <int KIND>
 cudaError_t launch_k(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  constexpr int D = KIND == KIND_COLLOC ? 1 : 2;
   switch (s.p) {
-    case 1: return launch_t<1, 1 + D, KIND>(s, a, st);
-    case 2: return launch_t<2, 2 + D, KIND>(s, a, st);
-    case 3: return launch_t<3, 3 + D, KIND>(s, a, st);
-    case 4: return launch_t<4, 4 + D, KIND>(s, a, st);
-    case 5: return launch_t<5, 5 + D, KIND>(s, a, st);
-    case 6: return launch_t<6, 6 + D, KIND>(s, a, st);
-    case 7: return launch_t<7, 7 + D, KIND>(s, a, st);
-    case 8: return launch_t<8, 8 + D, KIND>(s, a, st);
+    case 1: return launch_p<1, KIND>(s, a, st);
+    case 2: return launch_p<2, KIND>(s, a, st);
+    case 3: return launch_p<3, KIND>(s, a, st);
+    case 4: return launch_p<4, KIND>(s, a, st);
+    case 5: return launch_p<5, KIND>(s, a, st);
+    case 6: return launch_p<6, KIND>(s, a, st);
+    case 7: return launch_p<7, KIND>(s, a, st);
+    case 8: return launch_p<8, KIND>(s, a, st);
   }
   return cudaErrorInvalidValue;
 }

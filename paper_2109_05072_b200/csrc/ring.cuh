@@ -103,7 +103,8 @@ __device__ __forceinline__ double ring_node_sum(const double* latY, const double
 }
 
 // Global completion of a fused p.Ap: the last CTA sums the column partials in
-// index order and applies the CG scalar step. `coldot`: thread 0's column sum.
+// index order and applies the CG scalar step. `coldot`: thread 0's sum over the
+// CTA's columns; `col`: the CTA index (one partial per CTA).
 template <int NT>
 __device__ void ring_dot_finish(const ApplyArgs& A, int col, double coldot, double* red) {
   __shared__ int s_last;
@@ -117,7 +118,7 @@ __device__ void ring_dot_finish(const ApplyArgs& A, int col, double coldot, doub
   if (!s_last) return;
   __threadfence();
   double s = 0.0;
-  for (int c = threadIdx.x; c < A.ncols; c += NT) s += __ldcg(A.col_dot + c);
+  for (int c = threadIdx.x; c < static_cast<int>(gridDim.x); c += NT) s += __ldcg(A.col_dot + c);
   const double pAp = block_sum<NT>(s, red);
   if (threadIdx.x == 0) {
     *A.fix_done = 0;

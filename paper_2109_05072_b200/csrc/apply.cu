@@ -128,9 +128,10 @@ template <int P, int Q, int KIND, int SK>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int QQ = Q * Q;
+  static constexpr int GB = SK / 10000 ? 2 : 1;  // G staging buffers (2: issued one element ahead)
   static constexpr int S = SK / 10 % 10;  // lanes per pencil (1, 2, 4)
   static constexpr int KC = SK % 10;      // element columns per CTA
-  static constexpr int MAXREG = SK / 100 ? SK / 100 * 8 : 255;
+  static constexpr int MAXREG = SK / 100 % 100 ? SK / 100 % 100 * 8 : 255;
   static constexpr int RQ = (Q + S - 1) / S;      // quadrature rows per lane
   static constexpr int RN = (N + S - 1) / S;      // node outputs per lane (transposed phases)
   static constexpr int ZI = KC * N * N, YI = KC * N * Q, XI = KC * QQ;  // pencils per phase
@@ -145,9 +146,9 @@ struct Cfg {
   static constexpr int COMP = KIND == KIND_MASS ? 1 : 6;
   static constexpr int GS = (COMP * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
   static constexpr int G_OFF = KC * CB;                      // 16-byte aligned TMA destinations
-  static constexpr int U_OFF = G_OFF + KC * GS;              // per column two u slabs (cp.async double buffer)
+  static constexpr int U_OFF = G_OFF + GB * KC * GS;         // per column two u slabs (cp.async double buffer)
   static constexpr int BAR_OFF = U_OFF + KC * 2 * N * N * N;
-  static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
+  static constexpr int SMEM_BYTES = (BAR_OFF + GB) * 8;
 };
 
 // a[S r + s] for compile-time r and the lane's runtime s (0 past the end)
@@ -194,7 +195,7 @@ __device__ __forceinline__ void reduce_scatter(const double (&v)[L], double (&o)
 
 template <int P, int Q, int KIND, int SK, typename K_ = Cfg<P, Q, KIND, SK>>
 __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
-    bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs) {
+    bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
   using K = Cfg<P, Q, KIND, SK>;
   constexpr int N = K::N, QQ = K::QQ, NT = K::NT, S = K::S, KC = K::KC, RQ = K::RQ, RN = K::RN;
   constexpr bool COLLOC = KIND == KIND_COLLOC;
@@ -211,8 +212,16 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   const int wfirst = (t & ~31) / S;  // first pencil of this warp: whole-warp phase skips
   const uint64_t pol = policy_evict_first();
   const bool do_dot = A.col_dot != nullptr;
-  const int col0 = blockIdx.x * KC;
+  // CTA = (column group, z-segment). A segment recomputes the element below
+  // its first one without storing anything, so the carry hands it the full
+  // bottom node plane and it owns that plane outright (no cross-CTA sum).
+  const int ncta = (A.ncols + KC - 1) / KC;
+  const int seg = blockIdx.x / ncta;
+  const int col0 = (blockIdx.x - seg * ncta) * KC;
   const int kv = A.ncols - col0 < KC ? A.ncols - col0 : KC;  // valid columns of this CTA
+  const int z_lo = static_cast<int>(static_cast<long long>(seg) * A.nz / nseg);
+  const int z_hi = static_cast<int>(static_cast<long long>(seg + 1) * A.nz / nseg);
+  const int e0 = seg > 0 ? z_lo - 1 : z_lo;
 
   // basis rows of this lane: cB[r][i] = B(S r + s, i), cD likewise (0 past Q)
   double cB[RQ][N], cD[RQ][N];
@@ -255,18 +264,20 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   const double* Gcta = A.G + static_cast<long long>(col0) * gcol;
   if (t == 0) {
     mbar_init(bar, 1);
+    if constexpr (K::GB == 2) mbar_init(bar + 8, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue_g = [&](int ez) {  // thread 0
-    mbar_arrive_expect_tx(bar, gbytes * kv);
+  auto issue_g = [&](int ez, int buf) {  // thread 0
+    const uint32_t b = bar + 8 * buf;
+    mbar_arrive_expect_tx(b, gbytes * kv);
     for (int kk = 0; kk < kv; ++kk)
-      bulk_g2s(smem_u32(smem + K::G_OFF + kk * K::GS), Gcta + kk * gcol + ez * K::GS, gbytes, bar, pol);
+      bulk_g2s(smem_u32(smem + K::G_OFF + (buf * KC + kk) * K::GS), Gcta + kk * gcol + ez * K::GS, gbytes, b, pol);
   };
   if (t == 0) {
-    issue_g(0);
-    if (A.nz > 1)
-      for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + K::GS, gbytes);
+    issue_g(e0, 0);
+    if (e0 + 1 < z_hi)
+      for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + (e0 + 1) * K::GS, gbytes);
   }
   double* Uz = smem + K::U_OFF + kz * 2 * N * N * N + pz;  // this z-pencil's u staging (buffer 0)
   auto fetch_u = [&](int ez, int buf) {
@@ -283,24 +294,32 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     }
     cp_async_commit();
   };
-  fetch_u(0, 0);
+  fetch_u(e0, 0);
 
-  for (int ez = 0; ez < A.nz; ++ez) {
-    if (t == 0 && ez + 2 < A.nz)
+  for (int ez = e0; ez < z_hi; ++ez) {
+    const int le = ez - e0;  // element index within the CTA (buffer / barrier parity)
+    if (t == 0 && ez + 2 < z_hi)
       for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + (ez + 2) * K::GS, gbytes);
-    if (ez + 1 < A.nz) {
-      fetch_u(ez + 1, (ez + 1) & 1);
+    if (ez + 1 < z_hi) {
+      fetch_u(ez + 1, (le + 1) & 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     if constexpr (S > 1) __syncthreads();  // the lanes of a pencil fetched its nodes in turn
+    // two G buffers: element le+1's blocks stream while this element computes
+    // (its buffer was last read by phase X of element le-1, before the
+    // previous iteration's final barrier)
+    if (K::GB == 2 && t == 0 && ez + 1 < z_hi) {
+      fence_proxy_async();
+      issue_g(ez + 1, (le + 1) & 1);
+    }
 
     // ---------------- phase Z: gather the z-pencil, contract along z
     if (wfirst < K::ZI) {
       double* SA = smem + kz * K::CB;
       double uk[N];
-      const double* us = Uz + (ez & 1) * N * N * N;
+      const double* us = Uz + (le & 1) * N * N * N;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         const int Z = ez * P + k;
@@ -377,13 +396,14 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     __syncthreads();
 
     // ---------------- phase X: x-pencils, pointwise factors, back along x
-    mbar_wait_parity(bar, ez & 1);  // the G blocks have landed in shared memory
+    const int gbuf = K::GB == 2 ? (le & 1) : 0;
+    mbar_wait_parity(bar + 8 * gbuf, K::GB == 2 ? (le >> 1) & 1 : le & 1);  // the G blocks have landed
     if (wfirst < K::XI) {
       const bool act = item < K::XI;
       const int it = act ? item : K::XI - 1;
       const int kx = it / QQ, pp = it % QQ;
       double* SB = smem + kx * K::CB + K::SA_SIZE;
-      const double* Ge = smem + K::G_OFF + kx * K::GS;
+      const double* Ge = smem + K::G_OFF + (gbuf * KC + kx) * K::GS;
       if constexpr (MASS) {
         double x0[N], v[RQ];
 #pragma unroll
@@ -478,9 +498,9 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       }
     }
     __syncthreads();
-    if (t == 0 && ez + 1 < A.nz) {  // G buffers consumed: stream the next element's blocks
+    if (K::GB == 1 && t == 0 && ez + 1 < z_hi) {  // G buffers consumed: stream the next element's blocks
       fence_proxy_async();
-      issue_g(ez + 1);
+      issue_g(ez + 1, 0);
     }
 
     // ---------------- phase Y': back along y
@@ -575,8 +595,8 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       const double top = out[P / S];
       carry = S == 1 ? top : __shfl_sync(0xffffffffu, top, (t & 31) - s + P % S);
       const int kend = (ez == A.nz - 1) ? N : P;
-      const double* usz = Uz + (ez & 1) * N * N * N;  // u of this element, still staged
-      if (zvalid) {
+      const double* usz = Uz + (le & 1) * N * N * N;  // u of this element, still staged
+      if (zvalid && ez >= z_lo) {
         if (!do_dot) {  // plain apply: the lean epilogue
 #pragma unroll
           for (int r = 0; r < RN; ++r) {
@@ -685,6 +705,28 @@ int sk_select(int kind, int p, int dflt) {
   return c;
 }
 
+// z-segments per element column: enough CTAs for `waves` full waves of the
+// resident slots (148 SMs x occupancy), segments of at least `min_len`
+// elements (each segment recomputes one element). HEXBP_SEG_WAVES /
+// HEXBP_SEG_MIN override (dev A/B).
+int z_segments(int ncta, int occ, int nz) {
+  static int sms = 0;
+  static double waves = 2.0;
+  static int min_len = 4;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+    if (const char* v = std::getenv("HEXBP_SEG_WAVES")) waves = std::atof(v);
+    if (const char* v = std::getenv("HEXBP_SEG_MIN")) min_len = std::atoi(v) > 0 ? std::atoi(v) : 1;
+  }
+  const double want = waves * sms * occ;
+  if (ncta >= want) return 1;
+  int nseg = static_cast<int>((want + ncta - 1) / ncta);
+  const int cap = nz / min_len > 1 ? nz / min_len : 1;
+  return nseg < cap ? nseg : cap;
+}
+
 struct KInfo {
   void* fn;
   int nt;
@@ -722,7 +764,13 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
       bs.B[i][j] = s.B[i * (P + 1) + j];
       bs.D[i][j] = s.D[i * (P + 1) + j];
     }
-  bp_apply_kernel<P, Q, KIND, SK><<<(a.ncols + K::KC - 1) / K::KC, K::NT, K::SMEM_BYTES, st>>>(a, bs);
+  static int occ = 0;  // resident CTAs per SM, once per instantiation
+  if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bp_apply_kernel<P, Q, KIND, SK>, K::NT,
+                                                                K::SMEM_BYTES) != cudaSuccess)
+    occ = 1;
+  const int ncta = (a.ncols + K::KC - 1) / K::KC;
+  const int nseg = z_segments(ncta, occ, a.nz);
+  bp_apply_kernel<P, Q, KIND, SK><<<ncta * nseg, K::NT, K::SMEM_BYTES, st>>>(a, bs, nseg);
   return cudaGetLastError();
 }
 

@@ -343,7 +343,8 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
     al(reinterpret_cast<void**>(&w.lateral), sizeof(double) * (exact > fast ? exact : fast));
   }
   al(reinterpret_cast<void**>(&w.zupper), sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * s.dims[2]);
-  al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * ncols);
+  // one partial p.Ap per operator CTA: at most one per (column, z-segment) <= E
+  al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * static_cast<std::size_t>(ncols) * s.dims[2]);
   al(reinterpret_cast<void**>(&w.fix_partials), sizeof(double) * w.fixup_grid);
   al(reinterpret_cast<void**>(&w.fix_done), sizeof(unsigned int) * 4);
   al(reinterpret_cast<void**>(&w.sc), sizeof(DevScalars));

@@ -35,3 +35,27 @@ def test_fast_apply_and_fused_dot(bp, p):
     rr = hx.cg(A, b, xr, rel_tol=0.0, max_iter=8, mode="reference")
     np.testing.assert_allclose(rf.residual_history, rr.residual_history, rtol=1e-9)
     assert rel(xf, xr) <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bp,p", [(1, 3), (1, 8), (3, 4), (3, 8), (5, 5)])
+def test_z_segmented_columns(bp, p):
+    """Few columns, deep z: the kernel splits each column into z-segments
+    that recompute the element below them (apply.cu z_segments); results and
+    the fused CG dot must not change."""
+    dims = (2, 3, 24)
+    o = Oracle(bp, p, dims, 0.0)
+    mesh = hx.build_box_mesh(dims, p)
+    op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), mesh))
+    op.workspace().set_mode("fast")
+    u = random_vector(5 + p, o.n)
+    w = op.apply(u)
+    assert rel(w, o.apply(u, False)) <= TOL
+    assert rel(hx.ConstrainedOperator(op).apply(u), o.apply(u, True)) <= TOL
+    assert np.array_equal(op.apply(u), w)  # deterministic
+    A = hx.ConstrainedOperator(op) if bp != 1 else op
+    b = hx.bench_rhs(bp, p, dims)
+    xf, xr = np.zeros(op.size()), np.zeros(op.size())
+    rf = hx.cg(A, b, xf, rel_tol=0.0, max_iter=6, mode="fast")
+    rr = hx.cg(A, b, xr, rel_tol=0.0, max_iter=6, mode="reference")
+    np.testing.assert_allclose(rf.residual_history, rr.residual_history, rtol=1e-9)

@@ -319,8 +319,15 @@ struct RingUpdateArgs {
 
 // INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
 // r.r -> r0 and the stopping state, r.z -> rz (solver.hpp:102-124).
+#ifndef HX_RING_MINB
+#define HX_RING_MINB 8  // 64 warps per SM: latency hiding for the gathers (a small spill measured cheaper)
+#endif
+#ifndef HX_RING_U
+#define HX_RING_U 2
+#endif
+constexpr int RU = HX_RING_U;  // plain-row chunks of 32 nodes in flight per warp
 template <int P, bool INIT, bool PC>
-__global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_constant__ RingUpdateArgs R, double* part,
+__global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(const __grid_constant__ RingUpdateArgs R, double* part,
                                                                  unsigned int* done, DevScalars* sc, double* hist) {
   __shared__ double red[VT / 32];
   if (!INIT && *(volatile int*)&sc->status != ST_RUNNING) return;
@@ -343,12 +350,12 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
       // plain row: interior nodes read A p; x-face nodes X = fx*P sum the
       // (left, right) partial pair of latX (one 16-byte load)
       const double* xr = R.latX + L.x_index(R.nx, Z, Y, 0, 0);
-      for (int x0 = 0; x0 < R.Nx; x0 += 4 * 32) {
-        double a[4], rv[4];
-        double2 lr[4];
+      for (int x0 = 0; x0 < R.Nx; x0 += RU * 32) {
+        double a[RU], rv[RU];
+        double2 lr[RU];
         int xm = (x0 % P + lmod) % P;  // X % P for u = 0
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RU; ++u) {
           const int X = x0 + 32 * u + lane;
           const bool ok = X < R.Nx;
           const bool xface = ok && xm == 0;
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(VT) fused_ring_update_r_kernel(const __grid_co
           if (xm >= P) xm -= P;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RU; ++u) {
           const int X = x0 + 32 * u + lane;
           if (X < R.Nx) {
             const double v = INIT ? bb[X] - a[u] : fma(-alpha, a[u], rv[u]);

@@ -222,9 +222,19 @@ def main():
     if world > 1:
         from paper_2109_05072_b200 import parallel
 
-        res = parallel.bench_weak(bp, p, dims, K, W, args.amplitude)
+        res = parallel.bench_weak(bp, p, dims, K, W, args.amplitude, clock=lambda: ClockSampler(local))
         if rank != 0:
             return
+        b_op, b_it, nL, E = algorithmic_bytes(bp, p, dims)  # per GPU (its slab)
+        peak, peak_kind = load_peaks()
+        t_it = res["ms_per_step"] / 1e3
+        res["cg_iteration_roofline"] = {"algorithmic_bytes_per_iter_per_gpu": b_it,
+                                        "achieved_GBps_per_gpu": b_it / t_it / 1e9,
+                                        "frac": b_it / t_it / 1e9 / peak}
+        res["roofline"] = {"bound": "hbm", "achieved": b_it / t_it / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": b_it / t_it / 1e9 / peak, "traffic": None,
+                           "note": "whole CG iteration per GPU (N > 1 runs time no separate kernel)",
+                           "peak_source": f"{peak_kind} hbm_gbs"}
         print(json.dumps(res), flush=True)
         return
 

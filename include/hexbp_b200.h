@@ -216,6 +216,21 @@ int hexbp_cgd_report(hexbp_workspace_t ws, int* status, hexbp_cg_report* report,
  * nodes keep u when constrained. */
 int hexbp_plane_combine(double* dst_dev, const double* src_dev, const double* u_dev, int nxn, int nyn, int constrained,
                         void* stream);
+/* Fused z-slab iteration (fast mode; the single-GPU fast CG split at its two
+ * global reductions):
+ *   hexbp_cgd_apply_fused -> halo (plane exchange + hexbp_plane_combine on Ap)
+ *   -> all-gather -> hexbp_cgd_finish(PAP) -> hexbp_cgd_update_r_fused ->
+ *   all-gather -> hexbp_cgd_finish(UPDATE_R) -> hexbp_cgd_update_xp.
+ * apply_fused: Ap = A p (workspace p) with this rank's share of p.Ap in
+ * *partial_dev, fused into the operator kernel (the shares of the shared node
+ * planes add up across ranks by linearity; constrained nodes of plane 0 count
+ * on the rank below); the ring nodes of the shared planes are summed locally
+ * so that Ap holds this rank's partial plane for the halo exchange. */
+int hexbp_cgd_apply_fused(hexbp_setup_t setup, hexbp_workspace_t ws, int constrained, double* partial_dev,
+                          void* stream);
+/* r -= alpha Ap with the ring sums fused (shared planes read from the
+ * halo-summed Ap); this rank's r.r over owned nodes -> *partial_dev. */
+int hexbp_cgd_update_r_fused(hexbp_workspace_t ws, int constrained, double* partial_dev, void* stream);
 
 /* Kernel resource report: registers/thread, static+dynamic smem bytes,
  * threads per CTA, resident CTAs per SM. */

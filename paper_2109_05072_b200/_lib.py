@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
         "hexbp_cgd_update_xp": (C.c_int, [_vp, _vp, _vp]),
         "hexbp_cgd_report": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(CGReportC), _dp, C.c_int]),
         "hexbp_plane_combine": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
+        "hexbp_cgd_apply_fused": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+        "hexbp_cgd_update_r_fused": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     }
     dev_override = bool(os.environ.get("HEXBP_LIB"))  # A/B timing of older builds (tools/ab_time.py)
     for name, (res, args) in sig.items():

@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
                 lat[Z * lat_stride] = out[r];
                 // column-local share of p.Ap on the ring (ring.cuh); w = u rows counted once
                 if (bcxy || zbc)
-                  dot = owner ? fma(uv, uv, dot) : dot;
+                  dot = (owner && !(A.zlo_shared && Z == 0)) ? fma(uv, uv, dot) : dot;
                 else
                   dot = fma(uv, out[r], dot);
               } else {
@@ -652,14 +652,16 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
 // into its r-update, cg.cu; p.Ap is complete after part 1.)
 constexpr int FT = 256;
 
-__global__ void __launch_bounds__(FT) lateral_fixup_kernel(const __grid_constant__ ApplyArgs A, int P) {
+__global__ void __launch_bounds__(FT) lateral_fixup_kernel(const __grid_constant__ ApplyArgs A, int P, int z_begin,
+                                                          int z_end) {
   // one warp per node row (Y, Z): ring rows (Y % P == 0) finish every node,
   // other rows their x-face nodes X = fx*P
   const LatLayout L(P, A.nx, A.ny);
   const int lane = threadIdx.x & 31;
-  const long long rows = static_cast<long long>(A.Ny) * A.Nz;
-  for (long long row = blockIdx.x * (FT / 32) + (threadIdx.x >> 5); row < rows;
-       row += static_cast<long long>(gridDim.x) * (FT / 32)) {
+  const long long rows = static_cast<long long>(A.Ny) * (z_end - z_begin);
+  for (long long rr = blockIdx.x * (FT / 32) + (threadIdx.x >> 5); rr < rows;
+       rr += static_cast<long long>(gridDim.x) * (FT / 32)) {
+    const long long row = rr + static_cast<long long>(A.Ny) * z_begin;
     const int Z = static_cast<int>(row / A.Ny), Y = static_cast<int>(row - static_cast<long long>(Z) * A.Ny);
     const bool yring = Y % P == 0;
     const int count = yring ? A.Nx : A.nx + 1;
@@ -895,6 +897,7 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.fix_done = ws.fix_done;
   a.sc = sc;
   a.dot_out = dot_out;
+  a.zlo_shared = s.z0 > 0;
   if (ws.multipass) {  // Backend::Multipass analog (reference arithmetic; CG reduces in cg.cu)
     if (dot_out || sc) return cudaErrorInvalidValue;
     return launch_apply_multipass(s, ws.mp_buf, u, w, constrained, st);
@@ -914,7 +917,30 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
     }
   }
   if (e != cudaSuccess || !finish_ring) return e;  // CG: the r-update sums the ring (cg.cu)
-  lateral_fixup_kernel<<<ws.fixup_grid, FT, 0, st>>>(a, s.p);
+  lateral_fixup_kernel<<<ws.fixup_grid, FT, 0, st>>>(a, s.p, 0, a.Nz);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lateral_fixup_planes(const Setup& s, const Workspace& ws, const double* u, double* w,
+                                        int constrained, int z_begin, int z_end, cudaStream_t st) {
+  ApplyArgs a{};
+  a.u = u;
+  a.w = w;
+  a.nx = s.dims[0];
+  a.ny = s.dims[1];
+  a.nz = s.dims[2];
+  a.Nx = s.dims[0] * s.p + 1;
+  a.Ny = s.dims[1] * s.p + 1;
+  a.Nz = s.dims[2] * s.p + 1;
+  a.constrained = constrained;
+  a.bc_zlo = s.bc_zlo;
+  a.bc_zhi = s.bc_zhi;
+  a.lateral = ws.lateral;
+  a.lat_x = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
+  const long long rows = static_cast<long long>(a.Ny) * (z_end - z_begin);
+  long long g = (rows + FT / 32 - 1) / (FT / 32);
+  if (g > 148 * 8) g = 148 * 8;
+  lateral_fixup_kernel<<<static_cast<int>(g < 1 ? 1 : g), FT, 0, st>>>(a, s.p, z_begin, z_end);
   return cudaGetLastError();
 }
 

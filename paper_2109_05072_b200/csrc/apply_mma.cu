@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(NT, 2)
         if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
         if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
           if (zbc || (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
-            if (ring_owner(P, i, G, ex, ey, A.nx, A.ny)) dot = fma(uv, uv, dot);  // w = u, counted once
+            if (ring_owner(P, i, G, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0))
+              dot = fma(uv, uv, dot);  // w = u, counted once
           } else {
             dot = fma(uv, o[q], dot);
           }

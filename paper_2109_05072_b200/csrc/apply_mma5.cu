@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(NT, 3)
     for (int k = 0; k < N; ++k) {
       const int Z = e * P + k;
       if (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)) {
-        if (do_dot && own_xy && (k < P || e == nz - 1)) dot = fma(us[k * US_KS], us[k * US_KS], dot);
+        if (do_dot && own_xy && (k < P || e == nz - 1) && !(A.zlo_shared && Z == 0))
+          dot = fma(us[k * US_KS], us[k * US_KS], dot);
         us[k * US_KS] = 0.0;
       }
     }

@@ -598,6 +598,30 @@ int hexbp_cgd_finish(hexbp_workspace_t wh, int op, const double* gathered, int w
   return HEXBP_OK;
 }
 
+int hexbp_cgd_apply_fused(hexbp_setup_t h, hexbp_workspace_t wh, int constrained, double* partial, void* stream) {
+  if (!h || !wh || !partial) return invalid("cgd_apply_fused: null argument");
+  Workspace& w = wh->w;
+  const Setup& s = h->s;
+  if (w.s != &s) return invalid("cgd_apply_fused: workspace belongs to another setup");
+  if (w.exact || w.multipass) return invalid("cgd_apply_fused: fast mode only");
+  DeviceGuard g(s.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(launch_apply(s, w, w.p, w.Ap, constrained, partial, nullptr, st, /*finish_ring=*/false));
+  const int Nz = s.dims[2] * s.p + 1;
+  if (s.z0 > 0) CK(launch_lateral_fixup_planes(s, w, w.p, w.Ap, constrained, 0, 1, st));
+  if (s.z0 + s.dims[2] < s.gdims[2]) CK(launch_lateral_fixup_planes(s, w, w.p, w.Ap, constrained, Nz - 1, Nz, st));
+  return HEXBP_OK;
+}
+
+int hexbp_cgd_update_r_fused(hexbp_workspace_t wh, int constrained, double* partial, void* stream) {
+  if (!wh || !partial) return invalid("cgd_update_r_fused: null argument");
+  Workspace& w = wh->w;
+  if (w.exact || w.multipass) return invalid("cgd_update_r_fused: fast mode only");
+  DeviceGuard g(w.device);
+  CK(launch_cgd_update_r_fused(w, constrained, partial, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
 int hexbp_cgd_update_xp(hexbp_workspace_t wh, double* x, void* stream) {
   if (!wh || !x) return invalid("null argument");
   DeviceGuard g(wh->w.device);

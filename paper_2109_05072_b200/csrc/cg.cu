@@ -315,6 +315,12 @@ struct RingUpdateArgs {
   int max_iter;
   double* r;
   int nx, ny, Nx, Ny, Nz, constrained, bc_zlo, bc_zhi;
+  // z-slab partition: node planes Z = 0 / Nz-1 shared with the rank below /
+  // above hold the assembled (halo-summed) A p in Ap; plane 0 belongs to the
+  // rank below (not in this rank's r.r). rank_partial != nullptr: the last
+  // block stores this rank's r.r there instead of running the scalar step.
+  int zlo_asm, zhi_asm;
+  double* rank_partial;
 };
 
 // INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
@@ -346,7 +352,21 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
     const double* dd = PC ? R.dv + static_cast<long long>(R.Nx) * row : nullptr;
     const double* bb = INIT ? R.b + static_cast<long long>(R.Nx) * row : nullptr;
     double* po = INIT ? R.pout + static_cast<long long>(R.Nx) * row : nullptr;
-    if (Y % P != 0) {
+    if ((Z == 0 && R.zlo_asm) || (Z == R.Nz - 1 && R.zhi_asm)) {
+      // shared node plane, already assembled in Ap (constrained nodes: A p = p)
+      const bool owned = !(Z == 0 && R.zlo_asm);
+      for (int X = lane; X < R.Nx; X += 32) {
+        const double a = ap[X];
+        const double v = INIT ? bb[X] - a : fma(-alpha, a, rr_[X]);
+        rr_[X] = v;
+        const double z = PC ? v / dd[X] : v;
+        if (owned) {
+          acc = fma(v, v, acc);
+          if (PC) acz = fma(v, z, acz);
+        }
+        if (INIT) po[X] = z;
+      }
+    } else if (Y % P != 0) {
       // plain row: interior nodes read A p; x-face nodes X = fx*P sum the
       // (left, right) partial pair of latX (one 16-byte load)
       const double* xr = R.latX + L.x_index(R.nx, Z, Y, 0, 0);
@@ -445,6 +465,13 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
   __threadfence();
   const double rr = tree_partials(part, gridDim.x, red);
   const double rz = PC ? tree_partials(part + gridDim.x, gridDim.x, red) : rr;
+  if (R.rank_partial) {  // z-slab CG: the ranks' partials are combined by cgd_finish_kernel
+    if (threadIdx.x == 0) {
+      *R.rank_partial = rr;
+      *done = 0;
+    }
+    return;
+  }
   if (INIT) {
     if (threadIdx.x == 0) {
       const double r0 = sqrt(rr);
@@ -616,7 +643,8 @@ cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st) {
 namespace {
 template <bool INIT>
 cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained, const double* p_applied,
-                          const double* b, double rel_tol, int max_iter) {
+                          const double* b, double rel_tol, int max_iter, int zlo_asm = 0, int zhi_asm = 0,
+                          double* rank_partial = nullptr) {
   const Setup& s = *ws.s;
   RingUpdateArgs R;
   R.Ap = ws.Ap;
@@ -637,6 +665,9 @@ cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int c
   R.constrained = constrained;
   R.bc_zlo = s.bc_zlo;
   R.bc_zhi = s.bc_zhi;
+  R.zlo_asm = zlo_asm;
+  R.zhi_asm = zhi_asm;
+  R.rank_partial = rank_partial;
   switch (s.p) {
 #define HXB_RING_CASE(PP)                                                                                             \
   case PP:                                                                                                             \
@@ -670,6 +701,12 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
   }
   // fast mode: A p comes from launch_apply(..., finish_ring = false)
   return launch_ring_r<false>(ws, n, st, constrained, ws.p, nullptr, 0.0, 0);
+}
+
+cudaError_t launch_cgd_update_r_fused(const Workspace& ws, int constrained, double* rank_partial, cudaStream_t st) {
+  const Setup& s = *ws.s;
+  const int has_down = s.z0 > 0, has_up = s.z0 + s.dims[2] < s.gdims[2];
+  return launch_ring_r<false>(ws, s.nL, st, constrained, ws.p, nullptr, 0.0, 0, has_down, has_up, rank_partial);
 }
 
 cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const double* x, int64_t n, double rel_tol,

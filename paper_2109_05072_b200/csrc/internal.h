@@ -59,6 +59,8 @@ struct ApplyArgs {
   DevScalars* sc;           // CG scalars (nullptr: plain apply)
   double* dot_out;          // where the final dot lands (nullptr: CG alpha logic only)
   double* lat_x;            // fast mode: latX (ring.cuh)
+  int zlo_shared;           // z-slab partition: node plane Z = 0 is owned by the rank below (its
+                            // constrained nodes' u.u share of p.Ap is counted there)
 };
 
 struct Setup {
@@ -128,6 +130,12 @@ void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* 
 cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
                            cudaStream_t st);
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained = 1);
+// z-slab CG, fast mode: the r-update with the shared node planes already
+// assembled in Ap (halo-summed), r.r over owned nodes only -> *rank_partial
+cudaError_t launch_cgd_update_r_fused(const Workspace& ws, int constrained, double* rank_partial, cudaStream_t st);
+// transpose restriction part 2 for the node planes Z in [z_begin, z_end) only
+cudaError_t launch_lateral_fixup_planes(const Setup& s, const Workspace& ws, const double* u, double* w,
+                                        int constrained, int z_begin, int z_end, cudaStream_t st);
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st);
 // fast mode: r = b - A x with A x from launch_apply(x, ..., finish_ring = false)
 cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const double* x, int64_t n, double rel_tol,

@@ -112,6 +112,10 @@ class Comm:
         import torch
 
         src = self._stage(t)
+        if src.is_cuda:  # NCCL: one collective straight into the gathered vector
+            out = torch.empty(self.world * src.numel(), dtype=src.dtype, device=src.device)
+            self.dist.all_gather_into_tensor(out, src, group=self.group)
+            return out
         outs = [torch.empty_like(src) for _ in range(self.world)]
         self.dist.all_gather(outs, src, group=self.group)
         out = torch.cat(outs)
@@ -144,6 +148,9 @@ class CudaSlabOps:
         _check(_lib.lib().hexbp_workspace_vectors(self.ws._h, C.byref(r), C.byref(p), C.byref(ap)))
         self._ptr = {"r": r.value, "p": p.value, "Ap": ap.value}
         self.partial = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.partial2 = torch.zeros(1, dtype=torch.float64, device=self.device)
+        # fast mode: the fused iteration (operator with p.Ap, ring-summing r-update)
+        self.fused = mode == "fast"
 
     def _stream(self):
         return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -170,6 +177,18 @@ class CudaSlabOps:
     def finish(self, op, gathered, world, rel_tol, max_iter):
         _check(_lib.lib().hexbp_cgd_finish(self.ws._h, op, C.c_void_p(gathered.data_ptr()), world, rel_tol, max_iter,
                                            self._stream()))
+
+    def apply_fused(self, constrained):
+        """Ap = A p (workspace p) with this rank's p.Ap share -> self.partial;
+        shared planes locally assembled in Ap for the halo."""
+        _check(_lib.lib().hexbp_cgd_apply_fused(self.setup._h, self.ws._h, int(constrained),
+                                                C.c_void_p(self.partial.data_ptr()), self._stream()))
+        return self.partial
+
+    def update_r_fused(self, constrained):
+        _check(_lib.lib().hexbp_cgd_update_r_fused(self.ws._h, int(constrained),
+                                                   C.c_void_p(self.partial2.data_ptr()), self._stream()))
+        return self.partial2
 
     def update_xp(self, x):
         _check(_lib.lib().hexbp_cgd_update_xp(self.ws._h, C.c_void_p(_addr(x)), self._stream()))
@@ -249,11 +268,22 @@ def dist_cg(dop: DistributedOperator, b, x, rel_tol: float = 1e-8, max_iter: int
     p = ops.view("p")
     dop.apply(x, Ap, constrained)  # r0 = b - A x0
     ops.finish(HEXBP_CGD_INIT, comm.allgather_scalar(ops.reduce(HEXBP_CGD_INIT, b)), comm.world, rel_tol, max_iter)
+    fused = getattr(ops, "fused", False)
     for k in range(1, max_iter + 1):
-        dop.apply(p, Ap, constrained)
-        ops.finish(HEXBP_CGD_PAP, comm.allgather_scalar(ops.reduce(HEXBP_CGD_PAP)), comm.world, rel_tol, max_iter)
-        ops.finish(HEXBP_CGD_UPDATE_R, comm.allgather_scalar(ops.reduce(HEXBP_CGD_UPDATE_R)), comm.world, rel_tol,
-                   max_iter)
+        if fused:
+            # the single-GPU fast iteration split at its two reductions: p.Ap
+            # inside the operator kernel, ring sums inside the r-update
+            pap = ops.apply_fused(constrained)
+            dop.halo(p, Ap, constrained)
+            ops.finish(HEXBP_CGD_PAP, comm.allgather_scalar(pap), comm.world, rel_tol, max_iter)
+            rr = ops.update_r_fused(constrained)
+            ops.finish(HEXBP_CGD_UPDATE_R, comm.allgather_scalar(rr), comm.world, rel_tol, max_iter)
+        else:
+            dop.apply(p, Ap, constrained)
+            ops.finish(HEXBP_CGD_PAP, comm.allgather_scalar(ops.reduce(HEXBP_CGD_PAP)), comm.world, rel_tol,
+                       max_iter)
+            ops.finish(HEXBP_CGD_UPDATE_R, comm.allgather_scalar(ops.reduce(HEXBP_CGD_UPDATE_R)), comm.world,
+                       rel_tol, max_iter)
         ops.update_xp(x)
         if rel_tol > 0.0 and k % check_every == 0 and k < max_iter and ops.status() != ST_RUNNING:
             break
@@ -262,8 +292,12 @@ def dist_cg(dop: DistributedOperator, b, x, rel_tol: float = 1e-8, max_iter: int
     return rep
 
 
-def bench_weak(bp: int, p: int, dims, K: int, W: int, amplitude: float = 0.0) -> dict:
-    """Weak scaling: each rank owns a dims-sized slab of a (ex, ey, world*ez) box."""
+def bench_weak(bp: int, p: int, dims, K: int, W: int, amplitude: float = 0.0, clock=None) -> dict:
+    """Weak scaling: each rank owns a dims-sized slab of a (ex, ey, world*ez) box.
+    `clock`: optional context-manager factory sampling SM clocks around the
+    timed region (bench.py's ClockSampler)."""
+    import contextlib
+
     import torch
     import torch.distributed as dist
 
@@ -279,20 +313,42 @@ def bench_weak(bp: int, p: int, dims, K: int, W: int, amplitude: float = 0.0) ->
     dop = DistributedOperator(part, comm, ops)
     from .api import bench_rhs
 
-    b = torch.from_numpy(bench_rhs(bp, p, gdims, offset=part.global_offset, count=part.n_local)).cuda(local)
+    b_host = torch.from_numpy(bench_rhs(bp, p, gdims, offset=part.global_offset, count=part.n_local))
+    b = b_host.cuda(local)
     x = torch.zeros_like(b)
     dist_cg(dop, b, x, 0.0, W, constrained=bp != 1)
     x.zero_()
     torch.cuda.synchronize()
     dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    rep = dist_cg(dop, b, x, 0.0, K, constrained=bp != 1)
-    ev1.record()
-    torch.cuda.synchronize()
+    with (clock() if clock else contextlib.nullcontext()) as clk:
+        ev0.record()
+        rep = dist_cg(dop, b, x, 0.0, K, constrained=bp != 1)
+        ev1.record()
+        torch.cuda.synchronize()
     dist.barrier()
     t = comm.max_scalar(ev0.elapsed_time(ev1) / 1e3)
     value = part.n_global * K / t / 1e9
+
+    # end to end with host buffers: this rank's b slice in (pinned), x out, copies timed
+    bh = b_host.pin_memory()
+    xh = torch.empty(part.n_local, dtype=torch.float64).pin_memory()
+    x.zero_()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0.record()
+    b.copy_(bh, non_blocking=True)
+    dist_cg(dop, b, x, 0.0, K, constrained=bp != 1)
+    xh.copy_(x, non_blocking=True)
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    te = comm.max_scalar(ev0.elapsed_time(ev1) / 1e3)
+    planes = int(part.has_up) + int(part.has_down)
+    # our kernels per fused iteration: operator, shared-plane ring sums and halo
+    # combines, finish(PAP), r-update, finish(UPDATE_R), x/p update; plus the
+    # unfused initial residual (operator, ring fix-up, plane combines, reduce, finish)
+    launches = K * (5 + 2 * planes) + 4 + planes
     return {
         "metric": "BP3 GDOF/s (DOFs x CG iters/sec), fp64, % HBM roofline", "value": value, "unit": "GDOF/s",
         "n_gpus": comm.world, "steps": K, "warmup": W, "ms_per_step": t / K * 1e3, "higher_is_better": True,
@@ -301,7 +357,12 @@ def bench_weak(bp: int, p: int, dims, K: int, W: int, amplitude: float = 0.0) ->
         "config": {"workload": f"bp{bp} Q_{p}: {dims[0]}x{dims[1]}x{dims[2]} elements per GPU, global box "
                                f"{gdims[0]}x{gdims[1]}x{gdims[2]}, {part.n_global} DOFs, {K} fixed CG iterations",
                    "bp": bp, "p": p, "dims_per_gpu": list(dims), "global_dims": list(gdims),
-                   "parallelism": f"z-slab x{comm.world}, NCCL halo + all-gather"},
-        "gpu_launches": None, "cg_report": {"iterations": rep.iterations,
-                                            "final_rel_residual": rep.final_rel_residual},
+                   "parallelism": f"z-slab x{comm.world}, NCCL halo + all-gather, fused CG iteration",
+                   "l2": "inputs larger than L2"},
+        "e2e": {"value": part.n_global * K / te / 1e9, "unit": "GDOF/s",
+                "h2d_bytes_per_step": part.n_global * 8 / K, "d2h_bytes_per_step": part.n_global * 8 / K,
+                "path": "dist_cg per rank: pinned b slice in, x slice out, copies inside the timed region"},
+        "gpu_launches": launches,
+        "clocks": clk.summary() if clk is not None and hasattr(clk, "summary") else None,
+        "cg_report": {"iterations": rep.iterations, "final_rel_residual": rep.final_rel_residual},
     }

@@ -379,6 +379,8 @@ def main():
         # five-pass (gather / grad / factor / grad^T / scatter) pipeline
         line["fusion_vs_multipass"] = {f"bp{bp_}_p{p_}": fusion_compare(bp_, p_, K, local)
                                        for bp_, p_ in ((3, 7), (5, 7), (3, 4))}
+        # BASELINE configs[4] (per GPU): BP3 p = 3, 5, 7 at ~50M DOFs, CG to 1e-8
+        line["bp3_cg_to_1e-8_50M"] = {str(p_): cg_to_tol(3, p_, local) for p_ in (3, 5, 7)}
     print(json.dumps(line), flush=True)
 
 
@@ -418,6 +420,43 @@ def p_sweep(bp: int, K: int, local: int, ps=(2, 3, 4, 5, 6, 8), dofs: float = 50
         except Exception as ex:
             out[str(p)] = {"error": str(ex)[:120]}
     return out
+
+
+def cg_to_tol(bp: int, p: int, local: int, dofs: float = 50_000_000, rel_tol: float = 1e-8,
+              max_iter: int = 6000):
+    """Time to solution of the fast CG (rel_tol, bench RHS, x0 = 0), CUDA events."""
+    import torch
+
+    import paper_2109_05072_b200 as hx
+
+    e = 1
+    while ((e + 1) * p + 1) ** 3 <= dofs:
+        e += 1
+    dims = (e, e, e)
+    try:
+        op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), hx.build_box_mesh(dims, p),
+                                                             device=local))
+        A = hx.ConstrainedOperator(op) if bp != 1 else op
+        b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda(local)
+        x = torch.zeros_like(b)
+        hx.cg(A, b, x, 0.0, 3, mode="fast")
+        x.zero_()
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        rep = hx.cg(A, b, x, rel_tol, max_iter, mode="fast")
+        eb.record()
+        torch.cuda.synchronize()
+        dt = ea.elapsed_time(eb) / 1e3
+        n = b.numel()
+        out = {"dims": list(dims), "dofs": n, "iterations": rep.iterations, "converged": bool(rep.converged),
+               "final_rel_residual": rep.final_rel_residual, "seconds": dt,
+               "GDOFps": n * max(rep.iterations, 1) / dt / 1e9}
+        del op, A, b, x
+        torch.cuda.empty_cache()
+        return out
+    except Exception as ex:
+        return {"error": str(ex)[:160]}
 
 
 def fusion_compare(bp: int, p: int, K: int, local: int, dofs: float = 30_000_000):

@@ -86,6 +86,23 @@ int hexbp_setup_get_info(hexbp_setup_t s, hexbp_setup_info* out);
 int hexbp_setup_basis(hexbp_setup_t s, double* B, double* D);
 /* Factors downloaded back into the reference AoS layout (validation). */
 int hexbp_setup_factors(hexbp_setup_t s, double* factors_aos);
+/* Finite-element helpers of the manufactured-solution Poisson check
+ * (acceptance_main.cpp:181-222; device, reference arithmetic). Element order
+ * e = ex + nx (ey + ny ez) (mesh.hpp:71-82), quadrature point order
+ * a + q (b + q c); all pointers are device memory.
+ *   factors_device: the factors in the reference AoS layout (E x q^3 x comp)
+ *   node_coords:    box setups only: out[c * l_size + node] = mesh.coords[node][c]
+ *                   (mesh.hpp:107-119), bitwise
+ *   interp_to_qpts: gather + elem_interp (restriction.hpp:55-65,
+ *                   tensor.hpp:141-153): L-vector -> E x q^3
+ *   interp_transpose: elem_interp_transpose + scatter_add (tensor.hpp:155-172,
+ *                   restriction.hpp:67-80): E x q^3 -> L-vector (overwritten)
+ * assemble_load (solver.hpp:207-239) = interp_transpose(wdetJ * f(x_q)) and
+ * discrete_l2_error (solver.hpp:256-300) compose them (api.py). */
+int hexbp_setup_factors_device(hexbp_setup_t s, double* out_dev, void* stream);
+int hexbp_setup_node_coords(hexbp_setup_t s, double* out_dev, void* stream);
+int hexbp_interp_to_qpts(hexbp_setup_t s, const double* v_dev, double* out_dev, void* stream);
+int hexbp_interp_transpose(hexbp_setup_t s, const double* vq_dev, double* out_dev, void* stream);
 
 /* Replaces OperatorHandle::make_workspace (operator.hpp:262): ticket/progress
  * flags, per-column partial sums, CG vectors and scalars. All device memory

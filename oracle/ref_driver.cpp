@@ -12,7 +12,9 @@
 //   - check_equivalence (72-case sweep)       (verify.hpp:50-108)
 // No reference source is copied here; the headers are #included from their
 // original location at build time.
+#include <cmath>
 #include <cstdint>
+#include <numbers>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -199,6 +201,41 @@ int ref_pcg(void* hv, int constrained, const double* b, double* x, const double*
   } catch (const divergence_error& e) {
     g_err = e.what();
     return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// The manufactured-solution Poisson problem of acceptance criterion 5
+// (proj/tests/acceptance/acceptance_main.cpp:181-200) driven through the
+// reference's API: u = sin(pi x) sin(pi y) sin(pi z) on the unit cube, f = 3 pi^2 u,
+// BP3 fused operator with the box-boundary constraint, consistent load
+// vector (assemble_load, solver.hpp:207-239) with essential rows zeroed,
+// Jacobi-preconditioned cg (1e-8, 2000), discrete L2 error
+// (solver.hpp:256-300). Outputs: the load vector b (after zeroing), the
+// solution x (n = (elems p + 1)^3 each, may be null), the error, iterations.
+int ref_poisson(int elems, int p, double* b_out, double* x_out, double* err, int* iterations) {
+  try {
+    const double pi = std::numbers::pi;
+    auto exact = [pi](double x, double y, double z) { return std::sin(pi * x) * std::sin(pi * y) * std::sin(pi * z); };
+    auto rhs = [pi, exact](double x, double y, double z) { return 3.0 * pi * pi * exact(x, y, z); };
+    const HexMesh mesh = build_box_mesh({elems, elems, elems}, p, {1, 1, 1}, 0.0);
+    auto setup = make_setup(BPKind::BP3, mesh);
+    const OperatorHandle op(Backend::Fused, setup);
+    const ConstrainedOperator cop(op, boundary_bcs(mesh));
+    const GeomFactors mass = mass_factors(mesh, setup->basis);
+    std::vector<double> b = assemble_load(mesh, setup->basis, mass, setup->restriction, rhs);
+    for (int d : cop.bcs().dofs) b[d] = 0.0;
+    auto apply = [&](std::span<const double> u, std::vector<double>& w) { cop.apply(u, w); };
+    std::vector<double> x(op.size(), 0.0);
+    const std::vector<double> diag = jacobi_diagonal(cop);
+    const CGReport report = cg(apply, b, x, 1e-8, 2000, &diag);
+    if (b_out) std::memcpy(b_out, b.data(), sizeof(double) * b.size());
+    if (x_out) std::memcpy(x_out, x.data(), sizeof(double) * x.size());
+    *iterations = report.iterations;
+    *err = discrete_l2_error(mesh, setup->basis, mass, setup->restriction, x, exact);
+    return report.converged ? 0 : 3;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;

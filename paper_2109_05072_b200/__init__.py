@@ -41,3 +41,14 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]
+from .fe import (  # noqa: F401,E402
+    assemble_load,
+    boundary_mask,
+    discrete_l2_error,
+    factors_device,
+    interp_to_qpts,
+    interp_transpose,
+    nodal_interpolant,
+    node_coords,
+    quadrature_points,
+)

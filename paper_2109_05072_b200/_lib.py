@@ -77,6 +77,10 @@ def lib() -> C.CDLL:
         "hexbp_cgd_report": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(CGReportC), _dp, C.c_int]),
         "hexbp_plane_combine": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
         "hexbp_cgd_apply_fused": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+        "hexbp_setup_factors_device": (C.c_int, [_vp, _vp, _vp]),
+        "hexbp_setup_node_coords": (C.c_int, [_vp, _vp, _vp]),
+        "hexbp_interp_to_qpts": (C.c_int, [_vp, _vp, _vp, _vp]),
+        "hexbp_interp_transpose": (C.c_int, [_vp, _vp, _vp, _vp]),
         "hexbp_cgd_update_r_fused": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     }
     dev_override = bool(os.environ.get("HEXBP_LIB"))  # A/B timing of older builds (tools/ab_time.py)

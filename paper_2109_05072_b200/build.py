@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhexbp_b200.so")
-SOURCES = ["apply.cu", "apply_exact.cu", "apply_mma.cu", "apply_mma5.cu", "cg.cu", "jacobi.cu", "multipass.cu", "setup.cu", "capi.cu", "basis.cpp"]
+SOURCES = ["apply.cu", "apply_exact.cu", "apply_mma.cu", "apply_mma5.cu", "cg.cu", "jacobi.cu", "multipass.cu", "fe_tools.cu", "setup.cu", "capi.cu", "basis.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

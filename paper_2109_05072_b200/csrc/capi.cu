@@ -167,6 +167,9 @@ int create_box(int bp, int p, const int gdims[3], int z0, int z1, const double e
   }
   ga.amplitude = amplitude;
   for (int d = 0; d < 3; ++d) ga.ext[d] = ext[d];
+  s.box = 1;
+  s.amplitude = amplitude;
+  for (int d = 0; d < 3; ++d) s.ext[d] = ext[d];
   bad = reinterpret_cast<unsigned long long*>(dbuf + tot);
   bad_det = dbuf + tot + 2;
   cudaMemcpy(dbuf, host.data(), sizeof(double) * tot, cudaMemcpyHostToDevice);
@@ -314,6 +317,61 @@ int hexbp_setup_factors(hexbp_setup_t h, double* aos) {
   if (!e) e = cudaMemcpy(aos, tmp, sizeof(double) * n, cudaMemcpyDeviceToHost);
   cudaFree(tmp);
   return cuda_status(e, "factors download");
+}
+
+int hexbp_setup_factors_device(hexbp_setup_t h, double* out, void* stream) {
+  if (!h || !out) return invalid("null argument");
+  DeviceGuard g(h->s.device);
+  CK(launch_factors_to_aos(h->s, out, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_setup_node_coords(hexbp_setup_t h, double* out, void* stream) {
+  if (!h || !out) return invalid("null argument");
+  const Setup& s = h->s;
+  if (!s.box) return invalid("node_coords: setup was not created from a box mesh");
+  DeviceGuard g(s.device);
+  constexpr double kPi = 3.141592653589793;
+  std::vector<double> host;
+  std::size_t off[6];
+  for (int d = 0; d < 3; ++d) {  // mesh.hpp:59-67,107-116 on the host, as at setup
+    const std::vector<double> ax = axis_node_coords(s.gdims[d], s.p, s.ext[d]);
+    off[2 * d] = host.size();
+    host.insert(host.end(), ax.begin(), ax.end());
+    off[2 * d + 1] = host.size();
+    for (double x : ax) host.push_back(std::sin(2.0 * kPi * x / s.ext[d]));
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* dbuf = nullptr;
+  CK(cudaMallocAsync(&dbuf, sizeof(double) * host.size(), st));
+  cudaError_t e = cudaMemcpyAsync(dbuf, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, st);
+  BoxGeometryArgs ga{};
+  ga.ax = dbuf + off[0];
+  ga.sx = dbuf + off[1];
+  ga.ay = dbuf + off[2];
+  ga.sy = dbuf + off[3];
+  ga.az = dbuf + off[4];
+  ga.sz = dbuf + off[5];
+  ga.amplitude = s.amplitude;
+  for (int d = 0; d < 3; ++d) ga.ext[d] = s.ext[d];
+  if (!e) e = launch_node_coords(s, ga, out, st);
+  if (!e) e = cudaStreamSynchronize(st);  // the host staging vector goes out of scope
+  cudaFreeAsync(dbuf, st);
+  return cuda_status(e, "node_coords");
+}
+
+int hexbp_interp_to_qpts(hexbp_setup_t h, const double* v, double* out, void* stream) {
+  if (!h || !v || !out) return invalid("null argument");
+  DeviceGuard g(h->s.device);
+  CK(launch_interp_to_qpts(h->s, v, out, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_interp_transpose(hexbp_setup_t h, const double* vq, double* out, void* stream) {
+  if (!h || !vq || !out) return invalid("null argument");
+  DeviceGuard g(h->s.device);
+  CK(launch_interp_transpose(h->s, vq, out, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
 }
 
 int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {

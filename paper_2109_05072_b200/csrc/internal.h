@@ -78,6 +78,11 @@ struct Setup {
   double D[kMaxQ * (kMaxP + 1)] = {};
   double qw[kMaxQ] = {};
   double* G = nullptr;  // device
+  // box meshes (hexbp_setup_create_box*): the mesh parameters, so that node
+  // coordinates can be regenerated on the device (fe_tools.cu)
+  int box = 0;
+  double ext[3] = {1.0, 1.0, 1.0};
+  double amplitude = 0.0;
 };
 
 struct Workspace {
@@ -176,6 +181,10 @@ cudaError_t launch_box_geometry(const Setup& s, const BoxGeometryArgs& g, unsign
                                 double* bad_det, cudaStream_t st);
 cudaError_t launch_factors_from_aos(const Setup& s, const double* aos, cudaStream_t st);
 cudaError_t launch_factors_to_aos(const Setup& s, double* aos, cudaStream_t st);
+// ---- fe_tools.cu: finite-element helpers of the Poisson check (solver.hpp:207-300)
+cudaError_t launch_node_coords(const Setup& s, const BoxGeometryArgs& g, double* out, cudaStream_t st);
+cudaError_t launch_interp_to_qpts(const Setup& s, const double* v, double* out, cudaStream_t st);
+cudaError_t launch_interp_transpose(const Setup& s, const double* vq, double* out, cudaStream_t st);
 
 // ---- basis.cpp (host)
 void gl_rule(int n, double* pts, double* wts);

@@ -206,6 +206,9 @@ int hexbp_count_flops(hexbp_setup_t s, uint64_t* mul, uint64_t* add);
  * boundary dofs zeroed for BP3/BP5. Generated with the same std::mt19937_64 /
  * uniform_real_distribution so the device solves the reference's system. */
 int hexbp_bench_rhs(int bp, int p, const int dims[3], uint64_t seed, int64_t offset, int64_t count, double* out);
+/* `count` draws of std::uniform_real_distribution<double>(lo, hi) over
+ * std::mt19937_64(seed): check_equivalence's probe vectors (verify.hpp:64-70). */
+int hexbp_uniform_stream(uint64_t seed, double lo, double hi, int64_t count, double* out);
 
 /* ---- Multi-GPU z-slab building blocks (paper_2109_05072_b200/parallel.py).
  * The reference has no distributed path; these split hexbp_cg at its

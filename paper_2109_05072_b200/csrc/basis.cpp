@@ -200,3 +200,17 @@ extern "C" int hexbp_bench_rhs(int bp, int p, const int dims[3], uint64_t seed, 
   }
   return HEXBP_OK;
 }
+
+// std::mt19937_64(seed) + uniform_real_distribution<double>(lo, hi): the
+// probe vectors of check_equivalence (verify.hpp:64-70), same libstdc++ draws.
+extern "C" int hexbp_uniform_stream(uint64_t seed, double lo, double hi, int64_t count, double* out) {
+  if (!out || count < 0 || !(lo < hi)) {
+    hxb::set_error("uniform_stream: invalid argument");
+    return HEXBP_INVALID_ARGUMENT;
+  }
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(lo, hi);
+  for (int64_t i = 0; i < count; ++i) out[i] = dist(rng);
+  return HEXBP_OK;
+}
+

@@ -16,7 +16,11 @@ Backends: the reference's names are accepted by the parser ("multipass",
                    the paper's cuda-ref comparison point), reference arithmetic.
 Timing uses CUDA events around each device-resident solve.
 
-    python -m paper_2109_05072_b200.harness config.json [--csv out.csv] [--plot out.dat]
+The CLI mirrors bench_main.cpp:
+    python -m paper_2109_05072_b200.harness [run] config.json [--csv out.csv] [--plot out.dat]
+    python -m paper_2109_05072_b200.harness verify [--p P] [--mesh EXxEYxEZ] [--bp bp1|bp3|bp5]
+    python -m paper_2109_05072_b200.harness model [--p-min 1] [--p-max 8] [--collocated]
+`verify` runs check_equivalence (verify.hpp:50-108) for the device backends.
 """
 from __future__ import annotations
 
@@ -27,7 +31,11 @@ import sys
 from dataclasses import dataclass, field
 from typing import List, Optional
 
-from .api import BPKind, ConstrainedOperator, OperatorHandle, Backend, bench_rhs, build_box_mesh, cg, make_setup
+import ctypes as C
+
+from . import _lib
+from .api import (BPKind, ConstrainedOperator, DegenerateElementError, OperatorHandle, Backend, _check, bench_rhs,
+                  build_box_mesh, cg, is_diffusion, make_setup, parse_bp, to_string)
 
 K_MAX_DEFORM_AMPLITUDE = 0.15  # mesh.hpp:53
 CSV_HEADER = ("bp,backend,p,q,elements,dofs,cg_iters,seconds,throughput,"
@@ -289,7 +297,170 @@ def emit_plotdata(records, f) -> None:
             i += 1
 
 
+# ---------------------------------------------------------------- verify
+K_EQUIVALENCE_TOL = 1e-12  # verify.hpp:15
+
+
+@dataclass
+class EquivalenceCase:
+    """verify.hpp:17-22"""
+
+    bp: BPKind = BPKind.BP1
+    p: int = 1
+    dims: tuple = (1, 1, 1)
+    amplitude: float = 0.0
+
+
+def default_equivalence_cases() -> List[EquivalenceCase]:
+    """verify.hpp:38-46: every BP, p = 1..4, three box shapes, undeformed and deformed."""
+    return [EquivalenceCase(bp, p, dims, a) for bp in (BPKind.BP1, BPKind.BP3, BPKind.BP5) for p in (1, 2, 3, 4)
+            for dims in ((1, 1, 1), (2, 2, 2), (3, 2, 1)) for a in (0.0, 0.1)]
+
+
+def _uniform_stream(seed: int, count: int):
+    import numpy as np
+
+    out = np.empty(count)
+    _check(_lib.lib().hexbp_uniform_stream(C.c_uint64(seed & (2**64 - 1)), -1.0, 1.0, count,
+                                           out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def check_equivalence(c: EquivalenceCase, num_vectors: int = 10, tol: float = K_EQUIVALENCE_TOL,
+                      seed: int = 2024, device: int = 0) -> dict:
+    """check_equivalence (verify.hpp:50-108) for the device backends. The
+    comparison operator is the device operator in reference arithmetic,
+    which equals the reference's Fused backend bit for bit
+    (tests/test_gpu_parity.py) -- the assembled Backend::Oracle matrix is not
+    part of the hot path. Compared: "cuda" (fast kernels) and "cuda-multipass";
+    the probes are the reference's (mt19937_64(seed ^ p << 32 ^ n), U(-1, 1))."""
+    import numpy as np
+
+    mesh = build_box_mesh(c.dims, c.p, (1.0, 1.0, 1.0), c.amplitude)
+    setup = make_setup(c.bp, mesh, device=device)
+    exact = OperatorHandle(Backend.Cuda, setup)
+    fast = OperatorHandle(Backend.Cuda, setup)
+    fast.workspace().set_mode("fast")
+    multi = OperatorHandle(Backend.CudaMultipass, setup)
+    n = exact.size()
+    draws = _uniform_stream(seed ^ (c.p << 32) ^ n, 2 * num_vectors * n)
+    res = {"max_rel_multipass": 0.0, "max_rel_fused": 0.0, "max_symmetry": 0.0, "nullspace_residual": 0.0,
+           "min_quadratic_form": float("inf")}
+    for trial in range(num_vectors):
+        u = draws[2 * trial * n:(2 * trial + 1) * n]
+        v = draws[(2 * trial + 1) * n:(2 * trial + 2) * n]
+        wo, wm, wf = exact.apply(u), multi.apply(u), fast.apply(u)
+        ref = float(np.sqrt(wo @ wo))
+        res["max_rel_multipass"] = max(res["max_rel_multipass"], float(np.linalg.norm(wm - wo)) / ref)
+        res["max_rel_fused"] = max(res["max_rel_fused"], float(np.linalg.norm(wf - wo)) / ref)
+        wv = fast.apply(v)
+        uav, vau = float(u @ wv), float(v @ wf)
+        res["max_symmetry"] = max(res["max_symmetry"],
+                                  abs(uav - vau) / (float(np.linalg.norm(wf)) * float(np.linalg.norm(v))))
+        if c.bp == BPKind.BP1:
+            res["min_quadratic_form"] = min(res["min_quadratic_form"], float(u @ wf) / float(u @ u))
+    ok = res["max_rel_multipass"] <= tol and res["max_rel_fused"] <= tol and res["max_symmetry"] <= tol
+    if is_diffusion(c.bp):
+        from .api import jacobi_diagonal
+
+        w1 = fast.apply(np.ones(n))
+        # |A 1|_inf / |A|_inf; without the assembled matrix max_i |A_ii| <= |A|_inf
+        # stands in for the norm (a stricter test than the reference's)
+        scale = float(np.abs(jacobi_diagonal(exact, device=False)).max())
+        res["nullspace_residual"] = float(np.abs(w1).max()) / max(scale, 1e-300)
+        ok = ok and res["nullspace_residual"] <= tol
+    else:
+        ok = ok and res["min_quadratic_form"] > 0.0
+    res["pass"] = ok
+    return res
+
+
+def parse_mesh_dims(s: str) -> tuple:
+    """bench_main.cpp:27-37"""
+    parts = s.split("x")
+    if len(parts) != 3 or not all(x.strip().lstrip("-").isdigit() for x in parts):
+        raise ConfigError("mesh must look like EXxEYxEZ, e.g. 2x2x2")
+    dims = tuple(int(x) for x in parts)
+    if any(d < 1 for d in dims):
+        raise ConfigError("mesh dimensions must be >= 1")
+    return dims
+
+
+def verify_command(p: Optional[int] = None, mesh: Optional[str] = None, bp: Optional[str] = None,
+                   device: int = 0, out=None) -> int:
+    """bench_main.cpp:60-104: same case filtering, per-case line and summary."""
+    out = out or sys.stdout
+    cases = default_equivalence_cases()
+    if p is not None:
+        if p < 1:
+            raise ConfigError("--p must be >= 1")
+        cases = [c for c in cases if c.p == p]
+        if not cases:  # degree outside the default sweep: test it directly
+            cases = [EquivalenceCase(k, p, (2, 2, 2), a) for k in (BPKind.BP1, BPKind.BP3, BPKind.BP5)
+                     for a in (0.0, 0.1)]
+    if mesh:
+        dims = parse_mesh_dims(mesh)
+        for c in cases:
+            c.dims = dims
+    if bp:
+        kind = parse_bp(bp)
+        cases = [c for c in cases if c.bp == kind]
+    all_pass, worst = True, 0.0
+    for c in cases:
+        tag = f"{to_string(c.bp):<4} p={c.p} mesh={c.dims[0]}x{c.dims[1]}x{c.dims[2]} a={c.amplitude:.2f}"
+        try:
+            r = check_equivalence(c, device=device)
+            rel = max(r["max_rel_fused"], r["max_rel_multipass"])
+            worst = max(worst, rel)
+            print(f"{tag}  rel={rel:.3e} sym={r['max_symmetry']:.3e} {'ok' if r['pass'] else 'FAIL'}", file=out)
+            all_pass = all_pass and r["pass"]
+        except DegenerateElementError as e:
+            print(f"{tag}  DEGENERATE: {e}", file=out)
+            all_pass = False
+    print(f"{len(cases)} cases, worst backend/oracle deviation {worst:.3e}, tolerance {K_EQUIVALENCE_TOL:.1e}: "
+          f"{'PASS' if all_pass else 'FAIL'}", file=out)
+    return 0 if all_pass else 1  # kExitVerifyFailed (bench_main.cpp:25)
+
+
+def model_command(p_min: int = 1, p_max: int = 8, collocated: bool = False, out=None) -> int:
+    """bench_main.cpp:106-117"""
+    out = out or sys.stdout
+    if p_min < 1 or p_max < p_min:
+        raise ConfigError("need 1 <= --p-min <= --p-max")
+    print("p,collocated,flops_per_elem,reads_per_elem,ai", file=out)
+    for p in range(p_min, p_max + 1):
+        m = cost_model(p, collocated)
+        print(f"{p},{1 if collocated else 0},{m[0]},{m[1]},{m[2]:.17g}", file=out)
+    return 0
+
+
 def main(argv=None) -> int:
+    argv = list(sys.argv[1:] if argv is None else argv)
+    if argv and argv[0] == "verify":
+        ap = argparse.ArgumentParser(prog="harness verify")
+        ap.add_argument("--p", type=int, default=None)
+        ap.add_argument("--mesh", default=None)
+        ap.add_argument("--bp", default=None)
+        ap.add_argument("--device", type=int, default=0)
+        a = ap.parse_args(argv[1:])
+        try:
+            return verify_command(a.p, a.mesh, a.bp, a.device)
+        except (ConfigError, ValueError) as e:
+            print(f"config error: {e}", file=sys.stderr)
+            return 2
+    if argv and argv[0] == "model":
+        ap = argparse.ArgumentParser(prog="harness model")
+        ap.add_argument("--p-min", type=int, default=1)
+        ap.add_argument("--p-max", type=int, default=8)
+        ap.add_argument("--collocated", action="store_true")
+        a = ap.parse_args(argv[1:])
+        try:
+            return model_command(a.p_min, a.p_max, a.collocated)
+        except ConfigError as e:
+            print(f"config error: {e}", file=sys.stderr)
+            return 2
+    if argv and argv[0] == "run":
+        argv = argv[1:]
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("config")
     ap.add_argument("--csv", default=None)

@@ -142,3 +142,44 @@ def test_run_bench_cuda_backends_and_reference_history():
     out2 = H.run_bench(H.parse_config({"bp": "bp1", "degrees": [1], "dims": [2, 2, 2], "backends": ["fused", "cuda"],
                                        "warmup_repeats": 0, "timed_repeats": 1}))
     assert len(out2.records) == 1 and len(out2.errors) == 1
+
+
+def test_model_and_mesh_parsing_cli():
+    """bench_main.cpp model / --mesh parsing mirrors (no GPU)."""
+    import io
+
+    from paper_2109_05072_b200 import harness as H
+
+    buf = io.StringIO()
+    assert H.model_command(1, 3, True, out=buf) == 0
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == "p,collocated,flops_per_elem,reads_per_elem,ai" and len(lines) == 4
+    assert lines[3].startswith("3,1,4032,448,")  # acceptance_main.cpp:159 (p=3 collocated)
+    assert H.parse_mesh_dims("3x2x1") == (3, 2, 1)
+    for bad in ("3x2", "0x1x1", "axbxc"):
+        with pytest.raises(H.ConfigError):
+            H.parse_mesh_dims(bad)
+    assert len(H.default_equivalence_cases()) == 72
+
+
+@pytest.mark.gpu
+def test_verify_command_on_gpu():
+    """bench verify (bench_main.cpp:60-104) for the device backends: the full
+    72-case sweep passes at the reference's 1e-12 tolerance."""
+    import io
+
+    from paper_2109_05072_b200 import harness as H
+
+    buf = io.StringIO()
+    rc = H.verify_command(out=buf)
+    out = buf.getvalue().splitlines()
+    assert len(out) == 73
+    # as in the reference's own sweep, bp5 p=3 on one a=0.1 element is
+    # degenerate (tests/golden/equivalence.json) and fails the verify run
+    bad = [line for line in out[:-1] if not line.endswith(" ok")]
+    assert len(bad) == 1 and bad[0].startswith("bp5  p=3 mesh=1x1x1 a=0.10  DEGENERATE: non-positive Jacobian"), bad
+    assert out[-1].startswith("72 cases, worst backend/oracle deviation") and out[-1].endswith("FAIL"), out[-1]
+    assert rc == 1
+    buf = io.StringIO()
+    assert H.verify_command(p=6, bp="bp5", out=buf) == 0  # degree outside the sweep: 2x2x2, a in {0, 0.1}
+    assert len(buf.getvalue().splitlines()) == 3

@@ -326,7 +326,7 @@ struct RingUpdateArgs {
 // INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
 // r.r -> r0 and the stopping state, r.z -> rz (solver.hpp:102-124).
 #ifndef HX_RING_MINB
-#define HX_RING_MINB 8  // 64 warps per SM: latency hiding for the gathers (a small spill measured cheaper)
+#define HX_RING_MINB 6  // 48 warps per SM at 40 registers (8: 32 registers spill; 1: 76 registers, 24 warps)
 #endif
 #ifndef HX_RING_U
 #define HX_RING_U 2
@@ -371,25 +371,19 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
       // (left, right) partial pair of latX (one 16-byte load)
       const double* xr = R.latX + L.x_index(R.nx, Z, Y, 0, 0);
       for (int x0 = 0; x0 < R.Nx; x0 += RU * 32) {
-        double a[RU], rv[RU];
+        // every load of the chunk is issued before the first use
+        double av[RU], rv[RU];
         double2 lr[RU];
+        bool xf[RU];
         int xm = (x0 % P + lmod) % P;  // X % P for u = 0
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
           const int X = x0 + 32 * u + lane;
           const bool ok = X < R.Nx;
-          const bool xface = ok && xm == 0;
-          const bool bc = xface && R.constrained && (bcrow || X == 0 || X == R.Nx - 1);
+          xf[u] = ok && xm == 0;
           rv[u] = ok ? rr_[X] : 0.0;
-          a[u] = ok && !xface ? ap[X] : (bc ? pp[X] : 0.0);
-          lr[u] = xface && !bc ? __ldcg(reinterpret_cast<const double2*>(xr) + X / P) : make_double2(0.0, 0.0);
-          if (xface && !bc) {
-            const int fx = X / P;
-            double sum = 0.0;  // ascending column order (ring_node_sum)
-            if (fx > 0) sum += lr[u].x;
-            if (fx < R.nx) sum += lr[u].y;
-            a[u] = sum;
-          }
+          av[u] = ok && !xf[u] ? ap[X] : 0.0;
+          lr[u] = xf[u] ? __ldcg(reinterpret_cast<const double2*>(xr) + X / P) : make_double2(0.0, 0.0);
           xm += 32 % P;
           if (xm >= P) xm -= P;
         }
@@ -397,7 +391,19 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
         for (int u = 0; u < RU; ++u) {
           const int X = x0 + 32 * u + lane;
           if (X < R.Nx) {
-            const double v = INIT ? bb[X] - a[u] : fma(-alpha, a[u], rv[u]);
+            double a = av[u];
+            if (xf[u]) {
+              if (R.constrained && (bcrow || X == 0 || X == R.Nx - 1)) {
+                a = pp[X];  // ConstrainedOperator row: A p = p
+              } else {
+                const int fx = X / P;
+                double sum = 0.0;  // ascending column order (ring_node_sum)
+                if (fx > 0) sum += lr[u].x;
+                if (fx < R.nx) sum += lr[u].y;
+                a = sum;
+              }
+            }
+            const double v = INIT ? bb[X] - a : fma(-alpha, a, rv[u]);
             rr_[X] = v;
             acc = fma(v, v, acc);
             const double z = PC ? v / dd[X] : v;
@@ -414,37 +420,37 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
       const double* yb = R.latY + L.y_index(P, R.nx, Z, fy, 0, 0, 0);  // side 0 (column below)
       const double* ya = yb + static_cast<long long>(R.nx) * (P + 1);   // side 1 (column above)
       for (int x0 = 0; x0 < R.Nx; x0 += 2 * 32) {
-        double a[2], rv[2], q[2][4];
+        double rv[2], q[2][4];
         bool lo[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 2; ++u) {  // loads first
           const int X = x0 + 32 * u + lane;
           const bool ok = X < R.Nx;
-          const bool bc = ok && R.constrained && (bcrow || X == 0 || X == R.Nx - 1);
-          const bool need = ok && !bc;
           const int cxh = X / P < R.nx ? X / P : R.nx - 1;
           const int o = cxh * (P + 1) + (X - cxh * P);  // (cxh, ih) in a side's [cx][i] block
           lo[u] = X % P == 0 && X > 0 && X / P < R.nx;  // interior corner: (cxh-1, P) at o - 1
           rv[u] = ok ? rr_[X] : 0.0;
-          a[u] = bc ? pp[X] : 0.0;
-          q[u][0] = need && below && lo[u] ? __ldcg(yb + o - 1) : 0.0;
-          q[u][1] = need && below ? __ldcg(yb + o) : 0.0;
-          q[u][2] = need && above && lo[u] ? __ldcg(ya + o - 1) : 0.0;
-          q[u][3] = need && above ? __ldcg(ya + o) : 0.0;
-          if (need) {
-            double sum = 0.0;
-            if (below && lo[u]) sum += q[u][0];
-            if (below) sum += q[u][1];
-            if (above && lo[u]) sum += q[u][2];
-            if (above) sum += q[u][3];
-            a[u] = sum;
-          }
+          q[u][0] = ok && below && lo[u] ? __ldcg(yb + o - 1) : 0.0;
+          q[u][1] = ok && below ? __ldcg(yb + o) : 0.0;
+          q[u][2] = ok && above && lo[u] ? __ldcg(ya + o - 1) : 0.0;
+          q[u][3] = ok && above ? __ldcg(ya + o) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int X = x0 + 32 * u + lane;
           if (X < R.Nx) {
-            const double v = INIT ? bb[X] - a[u] : fma(-alpha, a[u], rv[u]);
+            double a;
+            if (R.constrained && (bcrow || X == 0 || X == R.Nx - 1)) {
+              a = pp[X];  // ConstrainedOperator row: A p = p
+            } else {
+              double sum = 0.0;  // ascending column order (ring_node_sum)
+              if (below && lo[u]) sum += q[u][0];
+              if (below) sum += q[u][1];
+              if (above && lo[u]) sum += q[u][2];
+              if (above) sum += q[u][3];
+              a = sum;
+            }
+            const double v = INIT ? bb[X] - a : fma(-alpha, a, rv[u]);
             rr_[X] = v;
             acc = fma(v, v, acc);
             const double z = PC ? v / dd[X] : v;

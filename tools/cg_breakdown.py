@@ -17,12 +17,15 @@ A = hx.ConstrainedOperator(op) if bp != 1 else op
 b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda()
 x = torch.zeros_like(b)
 hx.cg(A, b, x, 0.0, 3, mode="fast")
-for K in (5, 20):
+ts = []
+for rep in range(int(os.environ.get("REPS", "5"))):
     x.zero_()
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
-    hx.cg(A, b, x, 0.0, K, mode="fast")
+    hx.cg(A, b, x, 0.0, 20, mode="fast")
     ev[1].record()
     torch.cuda.synchronize()
-    print(f"K={K} total {ev[0].elapsed_time(ev[1]):.3f} ms", flush=True)
+    ts.append(ev[0].elapsed_time(ev[1]))
+ts.sort()
+print(f"K=20 min {ts[0]:.3f} median {ts[len(ts) // 2]:.3f} ms", flush=True)

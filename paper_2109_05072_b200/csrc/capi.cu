@@ -536,11 +536,7 @@ int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x,
   // Jacobi preconditioner for this solve (DevScalars::precond selects the
   // r.z recurrence of beta in the kernels' scalar logic)
   w.diag = diag;
-  {
-    const int pc = diag ? 1 : 0;
-    CK(cudaMemcpyAsync(reinterpret_cast<char*>(w.sc) + offsetof(DevScalars, precond), &pc, sizeof(int),
-                       cudaMemcpyHostToDevice, st));
-  }
+  CK(launch_set_int(&w.sc->precond, diag ? 1 : 0, st));
   struct ClearDiag {  // the workspace's other solvers (multi-GPU CG) run unpreconditioned
     Workspace& w;
     cudaStream_t st;
@@ -736,6 +732,8 @@ int hexbp_workspace_set_backend(hexbp_workspace_t wh, int backend) {
       w.mp_buf = nullptr;
       return cuda_status(cudaErrorMemoryAllocation, "multipass workspace");
     }
+    const cudaError_t e = launch_apply_multipass(*w.s, w.mp_buf, nullptr, nullptr, 0, nullptr, /*upload=*/true);
+    if (e != cudaSuccess) return cuda_status(e, "multipass basis upload");
   }
   w.multipass = backend == HEXBP_BACKEND_MULTIPASS;
   if (w.multipass) w.exact = 1;

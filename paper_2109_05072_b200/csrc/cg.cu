@@ -709,6 +709,13 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
   return launch_ring_r<false>(ws, n, st, constrained, ws.p, nullptr, 0.0, 0);
 }
 
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+cudaError_t launch_set_int(int* p, int v, cudaStream_t st) {
+  set_int_kernel<<<1, 1, 0, st>>>(p, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cgd_update_r_fused(const Workspace& ws, int constrained, double* rank_partial, cudaStream_t st) {
   const Setup& s = *ws.s;
   const int has_down = s.z0 > 0, has_up = s.z0 + s.dims[2] < s.gdims[2];

@@ -138,6 +138,8 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
 // z-slab CG, fast mode: the r-update with the shared node planes already
 // assembled in Ap (halo-summed), r.r over owned nodes only -> *rank_partial
 cudaError_t launch_cgd_update_r_fused(const Workspace& ws, int constrained, double* rank_partial, cudaStream_t st);
+// stream-ordered store of one int (a pageable cudaMemcpyAsync would synchronise the stream)
+cudaError_t launch_set_int(int* p, int v, cudaStream_t st);
 // transpose restriction part 2 for the node planes Z in [z_begin, z_end) only
 cudaError_t launch_lateral_fixup_planes(const Setup& s, const Workspace& ws, const double* u, double* w,
                                         int constrained, int z_begin, int z_end, cudaStream_t st);
@@ -150,8 +152,9 @@ cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const doub
 cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st);
 // ---- multipass.cu: apply_multipass (operator.hpp:318-394) on the GPU
 int64_t multipass_doubles(const Setup& s);
+// upload = true: store the basis tables into buf's tail (once, synchronous) and return
 cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u, double* w, int constrained,
-                                   cudaStream_t st);
+                                   cudaStream_t st, bool upload = false);
 // ---- jacobi.cu: jacobi_diagonal (solver.hpp:155-205) in reference arithmetic
 cudaError_t launch_jacobi_diagonal(const Setup& s, int constrained, double* diag, cudaStream_t st);
 int64_t reduction_partials(int64_t n);

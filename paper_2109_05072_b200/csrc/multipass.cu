@@ -190,7 +190,7 @@ int64_t multipass_doubles(const Setup& s) {
 }
 
 cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u, double* w, int constrained,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, bool upload) {
   MpCfg c{};
   c.p = s.p;
   c.n = s.p + 1;
@@ -226,11 +226,13 @@ cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u,
       Bt[i * q + a] = s.B[a * n + i];
       Dt[i * q + a] = s.D[a * n + i];
     }
-  cudaError_t e = cudaMemcpyAsync(dB, s.B, sizeof(double) * q * n, cudaMemcpyHostToDevice, st);
-  if (!e) e = cudaMemcpyAsync(dD, s.D, sizeof(double) * q * n, cudaMemcpyHostToDevice, st);
-  if (!e) e = cudaMemcpyAsync(dBt, Bt, sizeof(double) * q * n, cudaMemcpyHostToDevice, st);
-  if (!e) e = cudaMemcpyAsync(dDt, Dt, sizeof(double) * q * n, cudaMemcpyHostToDevice, st);
-  if (e) return e;
+  if (upload) {  // once, at hexbp_workspace_set_backend (a pageable copy synchronises the stream)
+    cudaError_t e = cudaMemcpy(dB, s.B, sizeof(double) * q * n, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(dD, s.D, sizeof(double) * q * n, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(dBt, Bt, sizeof(double) * q * n, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(dDt, Dt, sizeof(double) * q * n, cudaMemcpyHostToDevice);
+    return e;
+  }
   const size_t smg = sizeof(double) * (2 * q * n + nen + 2 * big * big * big + 3 * q3);
   const size_t smt = sizeof(double) * (2 * q * n + 3 * q3 + nen + 3 * big * big * big);
   static bool configured = false;

@@ -92,14 +92,103 @@ constexpr int best_stride(int N, int Q, int base, int kind) {
   return best;
 }
 
+// Even-odd form of a q x n basis matrix M on symmetric points,
+// M[q-1-a][n-1-i] = sg M[a][i] (sg = +1 for B, -1 for D): with e_i = x_i +
+// x_{n-1-i}, o_i = x_i - x_{n-1-i}, the pair (y_a, y_{q-1-a}) of y = M x is
+// (A + B, sg (A - B)), A = sum_i P[a][i] e_i (+ M[a][n/2] x_mid), B = sum_i
+// R[a][i] o_i -- half the multiply-adds and half the coefficients of the
+// plain product (the transposed product likewise). Fast mode only: it
+// rounds differently from the reference's loop order.
+template <int N, int Q>
+struct EOB {
+  static constexpr int NH = N / 2, QH = Q / 2;
+  double P[QH][NH];  // (M[a][i] + M[a][N-1-i]) / 2, a < q/2, i < n/2
+  double R[QH][NH];  // (M[a][i] - M[a][N-1-i]) / 2
+  double col[QH];    // M[a][n/2]      (n odd)
+  double row[NH];    // M[q/2][i]      (q odd)
+  double ctr;        // M[q/2][n/2]    (both odd)
+};
+
 template <int P, int Q>
 struct alignas(16) BasisT {  // 16-byte aligned kernel parameter: paired constant loads (LDCU.128)
   double B[Q][P + 1];
   double D[Q][P + 1];
+  EOB<P + 1, Q> eB, eD;
 };
 
+template <int N>
+__device__ __forceinline__ void eo_split(const double (&x)[N], double (&e)[N / 2], double (&o)[N / 2]) {
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    e[i] = x[i] + x[N - 1 - i];
+    o[i] = x[i] - x[N - 1 - i];
+  }
+}
+
+// y = M x, y_a handed to st(a, y_a)
+template <int SG, int N, int Q, class F>
+__device__ __forceinline__ void eo_fwd(const EOB<N, Q>& m, const double (&e)[N / 2], const double (&o)[N / 2],
+                                       const double (&x)[N], F&& st) {
+  constexpr int NH = N / 2, QH = Q / 2;
+#pragma unroll
+  for (int a = 0; a < QH; ++a) {
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int i = 0; i < NH; ++i) {
+      sa = fma(m.P[a][i], e[i], sa);
+      sb = fma(m.R[a][i], o[i], sb);
+    }
+    if constexpr (N & 1) sa = fma(m.col[a], x[NH], sa);
+    st(a, sa + sb);
+    st(Q - 1 - a, SG > 0 ? sa - sb : sb - sa);
+  }
+  if constexpr (Q & 1) {
+    double c = 0.0;
+#pragma unroll
+    for (int i = 0; i < NH; ++i) c = fma(m.row[i], SG > 0 ? e[i] : o[i], c);
+    if constexpr (N & 1) c = fma(m.ctr, x[NH], c);
+    st(QH, c);
+  }
+}
+
+// y (+)= M^T v
+template <int SG, bool ACC, int N, int Q>
+__device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q], double (&y)[N]) {
+  constexpr int NH = N / 2, QH = Q / 2;
+  double ve[QH], vo[QH];
+#pragma unroll
+  for (int a = 0; a < QH; ++a) {
+    ve[a] = SG > 0 ? v[a] + v[Q - 1 - a] : v[a] - v[Q - 1 - a];
+    vo[a] = SG > 0 ? v[a] - v[Q - 1 - a] : v[a] + v[Q - 1 - a];
+  }
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    double sp = 0.0, sq = 0.0;
+#pragma unroll
+    for (int a = 0; a < QH; ++a) {
+      sp = fma(m.P[a][i], ve[a], sp);
+      sq = fma(m.R[a][i], vo[a], sq);
+    }
+    double lo = sp + sq, hi = sp - sq;
+    if constexpr (Q & 1) {
+      lo = fma(m.row[i], v[QH], lo);
+      hi = SG > 0 ? fma(m.row[i], v[QH], hi) : fma(-m.row[i], v[QH], hi);
+    }
+    y[i] = ACC ? y[i] + lo : lo;
+    y[N - 1 - i] = ACC ? y[N - 1 - i] + hi : hi;
+  }
+  if constexpr (N & 1) {
+    double c = 0.0;
+#pragma unroll
+    for (int a = 0; a < QH; ++a) c = fma(m.col[a], ve[a], c);
+    if constexpr (Q & 1) c = fma(m.ctr, v[QH], c);
+    y[NH] = ACC ? y[NH] + c : c;
+  }
+}
+
 // Work split of the element kernel, per (P, KIND), as a code
-// SK = R*100 + S*10 + KC: S lanes share each pencil (lane s owns quadrature
+// SK = EO*100000 + G2*10000 + R*100 + S*10 + KC: EO = even-odd contractions
+// (EOB above), G2 = double-buffered G staging, S lanes share each pencil (lane s owns quadrature
 // rows s, s+S, ...; the transposed contractions' partial sums are
 // reduce-scattered by warp shuffles), KC element columns share a CTA, and
 // R*8 caps the registers (R = 0: 255). S divides the 2 Q (P+1) basis
@@ -107,9 +196,9 @@ struct alignas(16) BasisT {  // 16-byte aligned kernel parameter: paired constan
 // small. Values: measured per p on a B200 (profiles/README.md).
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
-  constexpr int mass[9] = {0, 18, 16, 16, 14, 13, 11, 11, 1611};
-  constexpr int diff[9] = {0, 17, 12, 13, 1812, 2111, 11, 11, 11};
-  constexpr int coll[9] = {0, 18, 13, 12, 12, 12, 12, 11, 11};
+  constexpr int mass[9] = {0, 18, 16, 100014, 100015, 100013, 100011, 100011, 100011};
+  constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 11, 100011};
+  constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 11, 100011};
   return kind == 0 ? mass[p] : kind == 1 ? diff[p] : coll[p];
 }
 // Candidate codes compiled for (KIND, P); the first is the default. A sweep
@@ -128,7 +217,8 @@ template <int P, int Q, int KIND, int SK>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int QQ = Q * Q;
-  static constexpr int GB = SK / 10000 ? 2 : 1;  // G staging buffers (2: issued one element ahead)
+  static constexpr bool EO = SK / 100000 % 10;   // even-odd contractions (requires S = 1)
+  static constexpr int GB = SK / 10000 % 10 ? 2 : 1;  // G staging buffers (2: issued one element ahead)
   static constexpr int S = SK / 10 % 10;  // lanes per pencil (1, 2, 4)
   static constexpr int KC = SK % 10;      // element columns per CTA
   static constexpr int MAXREG = SK / 100 % 100 ? SK / 100 % 100 * 8 : 255;
@@ -198,6 +288,8 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
   using K = Cfg<P, Q, KIND, SK>;
   constexpr int N = K::N, QQ = K::QQ, NT = K::NT, S = K::S, KC = K::KC, RQ = K::RQ, RN = K::RN;
+  constexpr int NH = N / 2;
+  static_assert(!K::EO || S == 1, "even-odd contractions need one lane per pencil");
   constexpr bool COLLOC = KIND == KIND_COLLOC;
   constexpr bool MASS = KIND == KIND_MASS;
 
@@ -327,6 +419,23 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
         uk[k] = v;
       }
+      if constexpr (K::EO) {
+        double e[NH], o[NH];
+        eo_split(uk, e, o);
+        if constexpr (COLLOC) {
+#pragma unroll
+          for (int c = 0; c < Q; ++c)
+            if (zrole) SA[c * K::SA_CS + pz] = uk[c];
+        } else {
+          eo_fwd<1>(bs.eB, e, o, uk, [&](int c, double v) {
+            if (zrole) SA[c * K::SA_CS + pz] = v;
+          });
+        }
+        if constexpr (!MASS)
+          eo_fwd<-1>(bs.eD, e, o, uk, [&](int c, double v) {
+            if (zrole) SA[(Q + c) * K::SA_CS + pz] = v;
+          });
+      } else
 #pragma unroll
       for (int r = 0; r < RQ; ++r) {
         const int c = S * r + s;
@@ -365,6 +474,33 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         if constexpr (!MASS) y1[j] = SA[(Q + c) * K::SA_CS + j * N + i];
       }
       double* sb = SB + i * K::SB_IS + c * Q;
+      if constexpr (K::EO) {
+        double e0[NH], o0[NH];
+        eo_split(y0, e0, o0);
+        if constexpr (COLLOC) {
+#pragma unroll
+          for (int b = 0; b < Q; ++b)
+            if (act) {
+              sb[b] = y0[b];
+              sb[2 * N * K::SB_IS + b] = y1[b];
+            }
+        } else {
+          eo_fwd<1>(bs.eB, e0, o0, y0, [&](int b, double v) {
+            if (act) sb[b] = v;
+          });
+          if constexpr (!MASS) {
+            double e1[NH], o1[NH];
+            eo_split(y1, e1, o1);
+            eo_fwd<1>(bs.eB, e1, o1, y1, [&](int b, double v) {
+              if (act) sb[2 * N * K::SB_IS + b] = v;
+            });
+          }
+        }
+        if constexpr (!MASS)
+          eo_fwd<-1>(bs.eD, e0, o0, y0, [&](int b, double v) {
+            if (act) sb[N * K::SB_IS + b] = v;
+          });
+      } else
 #pragma unroll
       for (int r = 0; r < RQ; ++r) {
         const int b = S * r + s;
@@ -404,7 +540,18 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       const int kx = it / QQ, pp = it % QQ;
       double* SB = smem + kx * K::CB + K::SA_SIZE;
       const double* Ge = smem + K::G_OFF + (gbuf * KC + kx) * K::GS;
-      if constexpr (MASS) {
+      if constexpr (MASS && K::EO) {
+        double x0[N], v[Q], out[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + pp];
+        double e[NH], o[NH];
+        eo_split(x0, e, o);
+        eo_fwd<1>(bs.eB, e, o, x0, [&](int a, double val) { v[a] = val * Ge[a * QQ + pp]; });
+        eo_bwd<1, false>(bs.eB, v, out);
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+          if (act) SB[i * K::SB_IS + pp] = out[i];
+      } else if constexpr (MASS) {
         double x0[N], v[RQ];
 #pragma unroll
         for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + pp];
@@ -430,7 +577,30 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           if (act && S * r + s < N) SB[(S * r + s) * K::SB_IS + pp] = o[r];
       } else {
         double gr[RQ], gs[RQ], gt[RQ];
-        {
+        if constexpr (K::EO) {
+          double x0[N], x1[N], x2[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            x0[i] = SB[i * K::SB_IS + pp];
+            x1[i] = SB[(N + i) * K::SB_IS + pp];
+            x2[i] = SB[(2 * N + i) * K::SB_IS + pp];
+          }
+          double e[NH], o[NH];
+          eo_split(x0, e, o);
+          eo_fwd<-1>(bs.eD, e, o, x0, [&](int a, double v) { gr[a] = v; });
+          if constexpr (COLLOC) {
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+              gs[a] = x1[a];
+              gt[a] = x2[a];
+            }
+          } else {
+            eo_split(x1, e, o);
+            eo_fwd<1>(bs.eB, e, o, x1, [&](int a, double v) { gs[a] = v; });
+            eo_split(x2, e, o);
+            eo_fwd<1>(bs.eB, e, o, x2, [&](int a, double v) { gt[a] = v; });
+          }
+        } else {
           double x0[N], x1[N], x2[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) {
@@ -476,6 +646,19 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
           double part[N], o[RN];
+          if constexpr (K::EO) {
+            if (f == 0) {
+              eo_bwd<-1, false>(bs.eD, gr, part);
+            } else if constexpr (COLLOC) {
+#pragma unroll
+              for (int i = 0; i < N; ++i) part[i] = f == 1 ? gs[i] : gt[i];
+            } else {
+              if (f == 1)
+                eo_bwd<1, false>(bs.eB, gs, part);
+              else
+                eo_bwd<1, false>(bs.eB, gt, part);
+            }
+          } else
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             double acc = 0.0;
@@ -523,6 +706,22 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         }
       }
       double p1[N], p2[N], o1[RN], o2[RN];
+      if constexpr (K::EO) {
+        if constexpr (MASS) {
+          eo_bwd<1, false>(bs.eB, a0, p1);
+        } else if constexpr (COLLOC) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            p1[j] = a0[j];
+            p2[j] = a2[j];
+          }
+          eo_bwd<-1, true>(bs.eD, a1, p1);
+        } else {
+          eo_bwd<1, false>(bs.eB, a0, p1);
+          eo_bwd<-1, true>(bs.eD, a1, p1);
+          eo_bwd<1, false>(bs.eB, a2, p2);
+        }
+      } else
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double c1 = 0.0, c2 = 0.0;
@@ -572,6 +771,15 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         if constexpr (!MASS) c2[r] = SA[(Q + cc) * K::SA_CS + pz];
       }
       double part[N], out[RN];
+      if constexpr (K::EO) {
+        if constexpr (COLLOC) {
+#pragma unroll
+          for (int k = 0; k < N; ++k) part[k] = c1[k];
+        } else {
+          eo_bwd<1, false>(bs.eB, c1, part);
+        }
+        if constexpr (!MASS) eo_bwd<-1, true>(bs.eD, c2, part);
+      } else
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double acc = 0.0;
@@ -755,6 +963,20 @@ KInfo info_t() {
   return info_sel<P, Q, KIND>(sk_select(KIND, P, SkList<KIND, P>::v[0]));
 }
 
+template <int N, int Q>
+void fill_eo(const double (&M)[Q][N], EOB<N, Q>& e) {
+  constexpr int NH = N / 2, QH = Q / 2;
+  for (int a = 0; a < QH; ++a) {
+    for (int i = 0; i < NH; ++i) {
+      e.P[a][i] = 0.5 * (M[a][i] + M[a][N - 1 - i]);
+      e.R[a][i] = 0.5 * (M[a][i] - M[a][N - 1 - i]);
+    }
+    e.col[a] = (N & 1) ? M[a][NH] : 0.0;
+  }
+  for (int i = 0; i < NH; ++i) e.row[i] = (Q & 1) ? M[QH][i] : 0.0;
+  e.ctr = ((N & 1) && (Q & 1)) ? M[QH][NH] : 0.0;
+}
+
 template <int P, int Q, int KIND, int SK>
 cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   using K = Cfg<P, Q, KIND, SK>;
@@ -766,6 +988,8 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
       bs.B[i][j] = s.B[i * (P + 1) + j];
       bs.D[i][j] = s.D[i * (P + 1) + j];
     }
+  fill_eo(bs.B, bs.eB);
+  fill_eo(bs.D, bs.eD);
   static int occ = 0;  // resident CTAs per SM, once per instantiation
   if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bp_apply_kernel<P, Q, KIND, SK>, K::NT,
                                                                 K::SMEM_BYTES) != cudaSuccess)

@@ -1068,14 +1068,10 @@ int fixup_grid(const Setup& s) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
-// DMMA kernel for BP3 p = 7 unless HEXBP_NO_DMMA=1 (A/B comparisons).
+// DMMA kernels for the setups whose factors are laid out for them (Setup::g_aos,
+// chosen at setup; HEXBP_NO_DMMA=1 there selects the DFMA layout for A/B runs).
 bool use_mma(const Setup& s) {
-  static const bool disabled = [] {
-    const char* v = std::getenv("HEXBP_NO_DMMA");
-    return v && *v && *v != '0';
-  }();
-  // the [qp][6] factor layout of BP3 p=7 setups is read by the DMMA kernel only
-  return (s.g_aos || !disabled) && (mma_kernel_applies(s) || mma5_kernel_applies(s));
+  return (s.g_aos == 1 && mma_kernel_applies(s)) || (s.g_aos == 2 && mma5_kernel_applies(s));
 }
 
 void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* blocks_per_sm) {

@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cstddef>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -98,7 +99,10 @@ int init_setup(Setup& s, int bp, int p, const int gdims[3], int z0, int z1, int 
   const long long per = static_cast<long long>(s.comp) * s.q * s.q * s.q;
   s.gstride = (per + 1) / 2 * 2;
   // DMMA kernels' factor block orders: [qp][6] (BP3 p=7, apply_mma.cu), [c][6][b][a] (BP5 p=7, apply_mma5.cu)
-  s.g_aos = (s.kind == KIND_DIFF && p == 7) ? 1 : ((s.kind == KIND_COLLOC && p == 7) ? 2 : 0);
+  // (HEXBP_NO_DMMA=1: the DFMA kernels' layout for A/B comparisons)
+  const char* no_dmma = std::getenv("HEXBP_NO_DMMA");
+  const bool dmma = !(no_dmma && *no_dmma && *no_dmma != '0');
+  s.g_aos = !dmma ? 0 : (s.kind == KIND_DIFF && p == 7) ? 1 : ((s.kind == KIND_COLLOC && p == 7) ? 2 : 0);
   std::vector<double> qp(s.q), npn(p + 1), nw(p + 1);
   try {
     build_basis(p, s.q, bp == 5, s.B, s.D, qp.data(), s.qw, npn.data(), nw.data());

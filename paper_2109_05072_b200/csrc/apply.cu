@@ -197,8 +197,9 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
   constexpr int mass[9] = {0, 18, 16, 100014, 100015, 100013, 100011, 100011, 100011};
-  constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 11, 100011};
-  constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 11, 100011};
+  // p = 7 BP3 / BP5 run the DMMA kernels; these entries serve HEXBP_NO_DMMA=1 setups
+  constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 102011, 100011};
+  constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 100011, 100011};
   return kind == 0 ? mass[p] : kind == 1 ? diff[p] : coll[p];
 }
 // Candidate codes compiled for (KIND, P); the first is the default. A sweep

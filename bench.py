@@ -349,7 +349,8 @@ def main():
                                   "frac": b_it * K / t_dev / 1e9 / peak,
                                   "roofline_GDOFps": peak * 1e9 / (b_it / nL) / 1e9},
         "e2e": {"value": e2e, "unit": "GDOF/s", "h2d_bytes_per_step": 2 * n * 8 / K, "d2h_bytes_per_step": n * 8 / K,
-                "path": "hexbp_cg_host (C ABI, pinned host b/x; b, x0 in and x out per solve, amortised per step)"},
+                "path": "hexbp_cg_host (C ABI, pinned host b/x; x0 in, then b in on a copy stream overlapping the initial "
+                        "A x0; x out; per solve, amortised per step)"},
         # per CG iteration: operator, ring-summing r-update, x/p update; plus the
         # initial residual (operator, ring-summing init)
         "gpu_launches": 3 * K + 2,

@@ -209,8 +209,29 @@ int ensure_host_staging(Workspace& w) {
   if (w.tmp_u) return HEXBP_OK;
   CK(cudaMalloc(&w.tmp_u, sizeof(double) * w.s->nL));
   CK(cudaMalloc(&w.tmp_w, sizeof(double) * w.s->nL));
+  CK(cudaStreamCreateWithFlags(&w.copy_st, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&w.ev_x, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&w.ev_b, cudaEventDisableTiming));
   return HEXBP_OK;
 }
+
+// Host-API staging of a solve's inputs: x0 first on the compute stream, then
+// b on the copy stream (after x0: the two would otherwise share PCIe and delay
+// the initial apply), so b's transfer overlaps the initial A x0. Returns the
+// event the residual kernel waits on.
+cudaError_t stage_solve_inputs(Workspace& w, const double* b, const double* x, int64_t n, cudaStream_t st) {
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  cudaError_t e = cudaMemcpyAsync(w.tmp_w, x, bytes, cudaMemcpyHostToDevice, st);
+  if (!e) e = cudaEventRecord(w.ev_x, st);
+  if (!e) e = cudaStreamWaitEvent(w.copy_st, w.ev_x, 0);
+  if (!e) e = cudaMemcpyAsync(w.tmp_u, b, bytes, cudaMemcpyHostToDevice, w.copy_st);
+  if (!e) e = cudaEventRecord(w.ev_b, w.copy_st);
+  return e;
+}
+
+int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, double rel_tol,
+            int max_iter, int constrained, hexbp_cg_report* report, double* history, cudaStream_t st,
+            cudaEvent_t b_ready);
 
 }  // namespace
 
@@ -435,6 +456,9 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (w.host_sc) cudaFreeHost(w.host_sc);
+  if (w.copy_st) cudaStreamDestroy(w.copy_st);
+  if (w.ev_x) cudaEventDestroy(w.ev_x);
+  if (w.ev_b) cudaEventDestroy(w.ev_b);
   delete wh;
 }
 
@@ -513,9 +537,8 @@ int hexbp_pcg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, doubl
     CK(cudaMalloc(&dd, sizeof(double) * n));
     CK(cudaMemcpy(dd, diag, sizeof(double) * n, cudaMemcpyHostToDevice));
   }
-  CK(cudaMemcpy(w.tmp_u, b, sizeof(double) * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(w.tmp_w, x, sizeof(double) * n, cudaMemcpyHostToDevice));
-  rc = hexbp_pcg(h, wh, w.tmp_u, w.tmp_w, dd, rel_tol, max_iter, constrained, report, history, nullptr);
+  CK(stage_solve_inputs(w, b, x, n, nullptr));
+  rc = pcg_run(h, wh, w.tmp_u, w.tmp_w, dd, rel_tol, max_iter, constrained, report, history, nullptr, w.ev_b);
   if (dd) cudaFree(dd);
   if (rc == HEXBP_OK || rc == HEXBP_DIVERGENCE) CK(cudaMemcpy(x, w.tmp_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return rc;
@@ -523,13 +546,23 @@ int hexbp_pcg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, doubl
 
 int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, double rel_tol,
               int max_iter, int constrained, hexbp_cg_report* report, double* history, void* stream) {
+  return pcg_run(h, wh, b, x, diag, rel_tol, max_iter, constrained, report, history,
+                 static_cast<cudaStream_t>(stream), nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+
+int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, double rel_tol,
+            int max_iter, int constrained, hexbp_cg_report* report, double* history, cudaStream_t st,
+            cudaEvent_t b_ready) {
   if (!h || !wh || !b || !x) return invalid("cg: null argument");
   if (max_iter < 0) return invalid("cg: max_iter must be >= 0");
   const auto t0 = std::chrono::steady_clock::now();
   const Setup& s = h->s;
   Workspace& w = wh->w;
   DeviceGuard g(s.device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (max_iter + 1 > w.history_cap) {
     CK(cudaFree(w.history));
     w.history = nullptr;
@@ -552,9 +585,11 @@ int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x,
   // r0 = b - A x0 (solver.hpp:102-103); fast mode sums the ring in the init kernel
   if (w.exact) {
     CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
+    if (b_ready) CK(cudaStreamWaitEvent(st, b_ready, 0));
     CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
   } else {
     CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st, /*finish_ring=*/false));
+    if (b_ready) CK(cudaStreamWaitEvent(st, b_ready, 0));
     CK(launch_cg_init_ring(w, b, x, n, rel_tol, max_iter, constrained, st));
   }
   if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz = r0.z0 (solver.hpp:124)
@@ -597,6 +632,10 @@ int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x,
   return HEXBP_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 int hexbp_cg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, int64_t n, double rel_tol,
                   int max_iter, int constrained, hexbp_cg_report* report, double* history) {
   if (!h || !wh || !b || !x) return invalid("cg: null argument");
@@ -605,9 +644,8 @@ int hexbp_cg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double
   Workspace& w = wh->w;
   int rc = ensure_host_staging(w);
   if (rc) return rc;
-  CK(cudaMemcpy(w.tmp_u, b, sizeof(double) * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(w.tmp_w, x, sizeof(double) * n, cudaMemcpyHostToDevice));
-  rc = hexbp_cg(h, wh, w.tmp_u, w.tmp_w, rel_tol, max_iter, constrained, report, history, nullptr);
+  CK(stage_solve_inputs(w, b, x, n, nullptr));
+  rc = pcg_run(h, wh, w.tmp_u, w.tmp_w, nullptr, rel_tol, max_iter, constrained, report, history, nullptr, w.ev_b);
   if (rc == HEXBP_OK || rc == HEXBP_DIVERGENCE) CK(cudaMemcpy(x, w.tmp_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return rc;
 }

@@ -111,6 +111,9 @@ struct Workspace {
   double* mp_buf = nullptr;       // its E-vectors, quadrature fields and basis tables
   double* dot_result = nullptr;
   DevScalars* host_sc = nullptr;  // pinned mirror
+  // host-API solves: b streams in on copy_st while the initial A x0 runs
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_b = nullptr;
 };
 
 // ---- apply.cu

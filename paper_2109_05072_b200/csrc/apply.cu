@@ -187,8 +187,9 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 }
 
 // Work split of the element kernel, per (P, KIND), as a code
-// SK = EO*100000 + G2*10000 + R*100 + S*10 + KC: EO = even-odd contractions
-// (EOB above), G2 = double-buffered G staging, S lanes share each pencil (lane s owns quadrature
+// SK = TPC*1000000 + EO*100000 + G2*10000 + R*100 + S*10 + KC: EO = even-odd contractions
+// (EOB above), G2 = double-buffered G staging, TPC = the thread-per-column
+// kernel below (BP1 p = 1; SK/10 % 100 its min CTAs per SM), S lanes share each pencil (lane s owns quadrature
 // rows s, s+S, ...; the transposed contractions' partial sums are
 // reduce-scattered by warp shuffles), KC element columns share a CTA, and
 // R*8 caps the registers (R = 0: 255). S divides the 2 Q (P+1) basis
@@ -196,7 +197,7 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 // small. Values: measured per p on a B200 (profiles/README.md).
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
-  constexpr int mass[9] = {0, 18, 16, 100014, 100015, 100013, 100011, 100011, 100011};
+  constexpr int mass[9] = {0, 1000000, 16, 100014, 100015, 100013, 100011, 100011, 100011};
   // p = 7 BP3 / BP5 run the DMMA kernels; these entries serve HEXBP_NO_DMMA=1 setups
   constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 102011, 100011};
   constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 100011, 100011};
@@ -856,6 +857,196 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   ring_dot_finish<NT>(A, blockIdx.x, cdot, s_red);
 }
 
+// Thread-per-column element kernel for BP1 at p = 1 (n = 2, q = 3): one
+// thread marches one element column in z with the whole element in
+// registers -- 8 nodes, 27 quadrature values, the z-shared input and output
+// node planes carried across elements -- and no barrier per element (the
+// CTA-per-column kernel above pays five per element, which dominates at
+// p = 1). z-segments as in bp_apply_kernel; ring partials in the same
+// lateral layout (every p = 1 node is a ring node), so the consumers are
+// unchanged.
+constexpr int TPC_T = 128;
+
+template <int P, int Q, int MB>
+__global__ void __launch_bounds__(TPC_T, MB)
+    tpc_mass_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
+  constexpr int N = P + 1, N2 = N * N, Q3 = Q * Q * Q;
+  constexpr int GS = (Q3 + 1) / 2 * 2;
+  __shared__ double s_red[TPC_T / 32];
+  if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
+  const int ncta = (A.ncols + TPC_T - 1) / TPC_T;
+  const int seg = blockIdx.x / ncta;
+  const int col_raw = (blockIdx.x - seg * ncta) * TPC_T + threadIdx.x;
+  const bool valid = col_raw < A.ncols;
+  const int col = valid ? col_raw : A.ncols - 1;
+  const int ex = col % A.nx, ey = col / A.nx;
+  const int z_lo = static_cast<int>(static_cast<long long>(seg) * A.nz / nseg);
+  const int z_hi = static_cast<int>(static_cast<long long>(seg + 1) * A.nz / nseg);
+  const int e0 = seg > 0 ? z_lo - 1 : z_lo;
+  const bool do_dot = A.col_dot != nullptr;
+  const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+  const long long base = ex * P + static_cast<long long>(A.Nx) * (ey * P);
+  const LatLayout L(P, A.nx, A.ny);
+  const double* Gcol = A.G + static_cast<long long>(col) * A.nz * GS;
+
+  auto bcxy = [&](int i, int j) {
+    const int X = ex * P + i, Y = ey * P + j;
+    return A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+  };
+  auto zbc = [&](int Z) { return A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)); };
+  double uraw[N][N2];  // this element's u (unmasked), planes k = 0..P
+  auto load_plane = [&](int k, int Z) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) uraw[k][j * N + i] = A.u[base + i + static_cast<long long>(A.Nx) * j + plane * Z];
+  };
+  double carry[N2];
+#pragma unroll
+  for (int l = 0; l < N2; ++l) carry[l] = 0.0;
+  double dot = 0.0;
+  load_plane(0, e0 * P);
+  for (int ez = e0; ez < z_hi; ++ez) {
+#pragma unroll
+    for (int k = 1; k < N; ++k) load_plane(k, ez * P + k);
+    double g[GS];
+    const double2* gp = reinterpret_cast<const double2*>(Gcol + static_cast<long long>(ez) * GS);
+#pragma unroll
+    for (int m = 0; m < GS / 2; ++m) {
+      const double2 v = __ldg(gp + m);
+      g[2 * m] = v.x;
+      g[2 * m + 1] = v.y;
+    }
+    // masked input (ConstrainedOperator: P u)
+    double u[N][N2];
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int l = 0; l < N2; ++l)
+        u[k][l] = (bcxy(l % N, l / N) || zbc(ez * P + k)) ? 0.0 : uraw[k][l];
+    // interpolation to the quadrature points, x then y then z
+    double t1[N][N][Q];  // [k][j][a]
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) s = fma(bs.B[a][i], u[k][j * N + i], s);
+          t1[k][j][a] = s;
+        }
+    double t2[N][Q][Q];  // [k][b][a]
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int b = 0; b < Q; ++b)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) s = fma(bs.B[b][j], t1[k][j][a], s);
+          t2[k][b][a] = s;
+        }
+    double v[Q][Q][Q];  // [c][b][a] times the mass factor (operator.hpp:139-142)
+#pragma unroll
+    for (int c = 0; c < Q; ++c)
+#pragma unroll
+      for (int b = 0; b < Q; ++b)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(bs.B[c][k], t2[k][b][a], s);
+          v[c][b][a] = s * g[a * Q * Q + (b + Q * c)];  // device layout [a][b + q c] (setup.cu)
+        }
+    // back: z, y, x
+    double r2[N][Q][Q];
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int b = 0; b < Q; ++b)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < Q; ++c) s = fma(bs.B[c][k], v[c][b][a], s);
+          r2[k][b][a] = s;
+        }
+    double r1[N][N][Q];
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int b = 0; b < Q; ++b) s = fma(bs.B[b][j], r2[k][b][a], s);
+          r1[k][j][a] = s;
+        }
+    double o[N][N2];
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) s = fma(bs.B[a][i], r1[k][j][a], s);
+          o[k][j * N + i] = s;
+        }
+    // transpose restriction, part 1: z-carry, then every footprint node is a ring node
+#pragma unroll
+    for (int l = 0; l < N2; ++l) {
+      o[0][l] += carry[l];
+      carry[l] = o[P][l];
+    }
+    const int kend = (ez == A.nz - 1) ? N : P;
+    if (valid && ez >= z_lo) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (k < kend) {
+          const int Z = ez * P + k;
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              const int l = j * N + i;
+              const bool ring = i == 0 || i == P || j == 0 || j == P;
+              const double val = o[k][l];
+              if (ring) {
+                bool is_y = false;
+                const long long li = lat_store_index(L, P, A.nx, ex, ey, i, j, Z, is_y);
+                (is_y ? A.lateral : A.lat_x)[li] = val;
+                if (do_dot) {
+                  const double uv = uraw[k][l];
+                  if (bcxy(i, j) || zbc(Z)) {
+                    if (ring_owner(P, i, j, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0)) dot = fma(uv, uv, dot);
+                  } else {
+                    dot = fma(uv, val, dot);
+                  }
+                }
+              } else {
+                const long long node = base + i + static_cast<long long>(A.Nx) * j + plane * Z;
+                const double w = zbc(Z) ? uraw[k][l] : val;
+                A.w[node] = w;
+                if (do_dot) dot = fma(uraw[k][l], w, dot);
+              }
+            }
+        }
+      }
+    }
+    // the top input plane is the next element's bottom plane
+#pragma unroll
+    for (int l = 0; l < N2; ++l) uraw[0][l] = uraw[P][l];
+  }
+  const double cdot = do_dot ? block_sum<TPC_T>(dot, s_red) : 0.0;
+  ring_dot_finish<TPC_T>(A, blockIdx.x, cdot, s_red);
+}
+
 // Transpose restriction, part 2, for plain applies: every ring node sums its
 // 1-4 column partials in ascending column order (ring.cuh). (CG fuses this
 // into its r-update, cg.cu; p.Ap is complete after part 1.)
@@ -950,8 +1141,12 @@ KInfo info_sel(int sk) {
   using L = SkList<KIND, P>;
   if constexpr (I < L::n) {
     constexpr int c = L::v[I];
-    using K = Cfg<P, Q, KIND, c>;
-    if (sk == c) return {kernel_ptr<P, Q, KIND, c>(), K::NT, K::SMEM_BYTES, K::KC};
+    if constexpr (c / 1000000 % 10) {  // thread-per-column kernel
+      if (sk == c) return {reinterpret_cast<void*>(&tpc_mass_kernel<P, Q, c / 10 % 100>), TPC_T, 0, TPC_T};
+    } else {
+      using K = Cfg<P, Q, KIND, c>;
+      if (sk == c) return {kernel_ptr<P, Q, KIND, c>(), K::NT, K::SMEM_BYTES, K::KC};
+    }
     return info_sel<P, Q, KIND, I + 1>(sk);
   } else {
     return {nullptr, 0, 0, 1};
@@ -979,7 +1174,29 @@ void fill_eo(const double (&M)[Q][N], EOB<N, Q>& e) {
 }
 
 template <int P, int Q, int KIND, int SK>
+cudaError_t launch_tpc(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  static_assert(KIND == KIND_MASS && P == 1, "thread-per-column kernel: BP1, p = 1");
+  BasisT<P, Q> bs;
+  for (int i = 0; i < Q; ++i)
+    for (int j = 0; j <= P; ++j) {
+      bs.B[i][j] = s.B[i * (P + 1) + j];
+      bs.D[i][j] = s.D[i * (P + 1) + j];
+    }
+  static int occ = 0;
+  constexpr int MB = SK / 10 % 100;  // min CTAs per SM (register cap)
+  if (occ == 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tpc_mass_kernel<P, Q, MB>, TPC_T, 0) != cudaSuccess)
+    occ = 1;
+  const int ncta = (a.ncols + TPC_T - 1) / TPC_T;
+  const int nseg = z_segments(ncta, occ, a.nz);
+  tpc_mass_kernel<P, Q, MB><<<ncta * nseg, TPC_T, 0, st>>>(a, bs, nseg);
+  return cudaGetLastError();
+}
+
+template <int P, int Q, int KIND, int SK>
 cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  if constexpr (SK / 1000000 % 10) return launch_tpc<P, Q, KIND, SK>(s, a, st);
+  else {
   using K = Cfg<P, Q, KIND, SK>;
   kernel_ptr<P, Q, KIND, SK>();
   if (s.gstride != K::GS) return cudaErrorInvalidValue;
@@ -999,6 +1216,7 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   const int nseg = z_segments(ncta, occ, a.nz);
   bp_apply_kernel<P, Q, KIND, SK><<<ncta * nseg, K::NT, K::SMEM_BYTES, st>>>(a, bs, nseg);
   return cudaGetLastError();
+  }
 }
 
 template <int P, int Q, int KIND, int I = 0>

@@ -38,7 +38,7 @@ def test_fast_apply_and_fused_dot(bp, p):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("bp,p", [(1, 3), (1, 8), (3, 4), (3, 8), (5, 5)])
+@pytest.mark.parametrize("bp,p", [(1, 1), (1, 3), (1, 8), (3, 4), (3, 8), (5, 5)])
 def test_z_segmented_columns(bp, p):
     """Few columns, deep z: the kernel splits each column into z-segments
     that recompute the element below them (apply.cu z_segments); results and

@@ -352,8 +352,8 @@ def main():
                 "path": "hexbp_cg_host (C ABI, pinned host b/x; x0 in, then b in on a copy stream overlapping the initial "
                         "A x0; x out; per solve, amortised per step)"},
         # per CG iteration: operator, ring-summing r-update, x/p update; plus the
-        # initial residual (operator, ring-summing init)
-        "gpu_launches": 3 * K + 2,
+        # preconditioner flag store and the initial residual (operator, ring-summing init)
+        "gpu_launches": 3 * K + 3,
         "reference_mode": {"GDOFps": n * K / t_ref / 1e9, "ms_per_step": t_ref / K * 1e3,
                            "note": "bit-exact reference arithmetic (same iterates as the CPU reference)",
                            "final_rel_residual": rep_ref.final_rel_residual},

@@ -9,9 +9,11 @@
 // plus the ConstrainedOperator wrapper (solver.hpp:60-65) and, in CG mode,
 // the p.Ap reduction and alpha = rz / pAp (solver.hpp:127-131).
 //
-// Work decomposition ("element columns"): CTA c owns the (ex, ey) column of
-// elements and marches it along z. The structured-mesh gather is index
-// arithmetic (mesh.hpp:81); no connectivity table is read.
+// Work decomposition ("element columns"): a CTA owns KC element columns
+// (ex, ey) and marches them along z (optionally one z-segment of them, see
+// z_segments). The structured-mesh gather is index arithmetic (mesh.hpp:81);
+// no connectivity table is read. BP1 at p = 1 uses one thread per column
+// instead (tpc_mass_kernel).
 //
 // Deterministic transpose restriction (K4), one launch:
 //  1. z-shared node planes are summed in registers (carry of the previous
@@ -27,16 +29,17 @@
 // bitwise identical run to run (restriction.hpp:18-21) with no inter-CTA
 // waiting.
 //
-// Element pipeline (q x q threads per column, z-pencil -> y -> x pencils):
+// Element pipeline (one thread per pencil and column, z-pencil -> y -> x):
 //   Z : thread (i,j) holds u(i,j,:) in registers; B_z u, D_z u        -> smem A
 //   Y : thread (i,c) holds a y-pencil; B_y, D_y                         -> smem B
 //   X : thread (b,c) holds x-pencils; gr, gs, gt at the q points of its x-line,
-//       G streamed from HBM straight to registers (coalesced, L2 evict-first,
+//       times the factors G_e (TMA-staged in shared memory, L2 evict-first,
 //       bulk-prefetched two elements ahead), then D_x^T / B_x^T          -> smem B
 //   Y': B_y^T, D_y^T                                                     -> smem A
 //   Z': B_z^T, D_z^T into the z-pencil registers = the element's result.
-// The contraction order is the reference's (D,B,B),(B,D,B),(B,B,D) with the
-// shared sweeps of tensor.hpp:193-202 / 226-234.
+// Every 1D contraction is either the plain product or its even-odd form
+// (EOB, from p = 4); both round differently from the reference's loop order
+// (fast mode; apply_exact.cu is the bit-exact path).
 #include <cuda_runtime.h>
 
 #include <cstdint>

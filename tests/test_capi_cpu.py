@@ -40,6 +40,17 @@ def test_bench_rhs_matches_oracle_recipe():
         hx.bench_rhs(3, 3, (2, 2, 2), offset=10**6, count=1)
 
 
+def test_uniform_stream_is_the_verify_probe_stream():
+    """hexbp_uniform_stream (the device verify's probe vectors) = mt19937_64 +
+    uniform_real_distribution(-1, 1) as check_equivalence draws them
+    (verify.hpp:64-70); pinned to the oracle's restatement of that stream."""
+    from oracle import random_vector
+    from paper_2109_05072_b200 import harness as H
+
+    for seed, n in [(2024 ^ (3 << 32) ^ 125, 1000), (77, 17), (12345, 4096)]:
+        assert np.array_equal(H._uniform_stream(seed, n), random_vector(seed, n))
+
+
 def test_mesh_api_validation_mirrors_reference():
     with pytest.raises(ValueError, match="element counts"):
         hx.build_box_mesh((0, 1, 1), 2)

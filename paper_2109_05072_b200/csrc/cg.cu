@@ -326,7 +326,7 @@ struct RingUpdateArgs {
 // INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
 // r.r -> r0 and the stopping state, r.z -> rz (solver.hpp:102-124).
 #ifndef HX_RING_MINB
-#define HX_RING_MINB 6  // 48 warps per SM at 40 registers (8: 32 registers spill; 1: 76 registers, 24 warps)
+#define HX_RING_MINB 4  // 64 registers, no spill: the 16-byte plain-row path keeps 4 pairs in flight
 #endif
 #ifndef HX_RING_U
 #define HX_RING_U 2
@@ -370,6 +370,59 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
       // plain row: interior nodes read A p; x-face nodes X = fx*P sum the
       // (left, right) partial pair of latX (one 16-byte load)
       const double* xr = R.latX + L.x_index(R.nx, Z, Y, 0, 0);
+      if constexpr (!INIT && !PC) {
+        // the CG iteration's form with 16-byte accesses: node pairs (X, X+1)
+        // at even global index, the odd element at the row start / end alone
+        const int head = static_cast<int>((static_cast<long long>(R.Nx) * row) & 1);
+        auto lat_at = [&](int X) { return __ldcg(reinterpret_cast<const double2*>(xr) + X / P); };
+        auto node_a = [&](int X, double a_loaded, double2 lr) -> double {  // A p at node X of the row
+          if (X % P != 0) return a_loaded;
+          if (R.constrained && (bcrow || X == 0 || X == R.Nx - 1)) return pp[X];  // A p = p
+          const int fx = X / P;
+          double sum = 0.0;  // ascending column order (ring_node_sum)
+          if (fx > 0) sum += lr.x;
+          if (fx < R.nx) sum += lr.y;
+          return sum;
+        };
+        auto single = [&](int X) {
+          const bool xf = X % P == 0;
+          const double rv = rr_[X];
+          const double a = node_a(X, xf ? 0.0 : ap[X], xf ? lat_at(X) : make_double2(0.0, 0.0));
+          const double v = fma(-alpha, a, rv);
+          rr_[X] = v;
+          acc = fma(v, v, acc);
+        };
+        if (head && lane == 0) single(0);
+        const int npair = (R.Nx - head) / 2;
+        for (int k0 = 0; k0 < npair; k0 += RU * 32) {
+          double2 rv[RU], av[RU], l0[RU], l1[RU];
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {  // every load of the chunk before the first use
+            const int k = k0 + 32 * u + lane;
+            const bool ok = k < npair;
+            const int X = head + 2 * k;
+            const bool f0 = ok && X % P == 0, f1 = ok && (X + 1) % P == 0;
+            rv[u] = ok ? *reinterpret_cast<const double2*>(rr_ + X) : make_double2(0.0, 0.0);
+            av[u] = ok ? *reinterpret_cast<const double2*>(ap + X) : make_double2(0.0, 0.0);
+            l0[u] = f0 ? lat_at(X) : make_double2(0.0, 0.0);
+            l1[u] = f1 ? lat_at(X + 1) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {
+            const int k = k0 + 32 * u + lane;
+            if (k < npair) {
+              const int X = head + 2 * k;
+              const double a0 = node_a(X, av[u].x, l0[u]), a1 = node_a(X + 1, av[u].y, l1[u]);
+              const double2 v = make_double2(fma(-alpha, a0, rv[u].x), fma(-alpha, a1, rv[u].y));
+              *reinterpret_cast<double2*>(rr_ + X) = v;
+              acc = fma(v.x, v.x, acc);
+              acc = fma(v.y, v.y, acc);
+            }
+          }
+        }
+        const int tail = head + 2 * npair;
+        if (tail < R.Nx && lane == 0) single(tail);
+      } else
       for (int x0 = 0; x0 < R.Nx; x0 += RU * 32) {
         // every load of the chunk is issued before the first use
         double av[RU], rv[RU];

@@ -66,16 +66,19 @@ def _worker(rank, world, port, case, mode, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,mode", [((3, 7, (4, 3, 6), 0.1), "fast"), ((3, 3, (5, 4, 6), 0.1), "reference"),
-                                       ((5, 4, (3, 3, 4), 0.1), "fast")])
-def test_two_ranks_on_one_gpu_match_single_domain(case, mode):
+@pytest.mark.parametrize("world,case,mode", [(2, (3, 7, (4, 3, 6), 0.1), "fast"), (2, (3, 3, (5, 4, 6), 0.1), "reference"),
+                                             (2, (5, 4, (3, 3, 4), 0.1), "fast"), (3, (3, 5, (3, 2, 6), 0.1), "fast"),
+                                             (3, (1, 2, (2, 3, 6), 0.0), "fast")])
+def test_ranks_on_one_gpu_match_single_domain(world, case, mode):
+    """world = 3: the middle rank has both a lower and an upper shared plane
+    (fused iteration: local plane ring sums, ownership of plane 0)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, mode, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    res = dict(q.get(timeout=600) for _ in range(2))
+    res = dict(q.get(timeout=600) for _ in range(world))
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0

@@ -1093,21 +1093,18 @@ void* kernel_ptr() {
   return reinterpret_cast<void*>(&bp_apply_kernel<P, Q, KIND, SK>);
 }
 
-// the SK code in use for (kind, p): the default, or HEXBP_SK_<kind>_<p> when
-// a sweep build compiled that candidate
+// the SK code in use for (kind, p): the default; sweep builds (tools/sk_sweep.py)
+// read HEXBP_SK_<kind>_<p> at every launch to select one of their compiled candidates
 int sk_select(int kind, int p, int dflt) {
-  static int cache[3][9] = {};
-  int& c = cache[kind][p];
 #ifdef HX_SK_SWEEP
-  c = 0;  // sweep builds re-read the environment at every launch
+  char name[32];
+  std::snprintf(name, sizeof(name), "HEXBP_SK_%d_%d", kind, p);
+  if (const char* v = std::getenv(name)) return std::atoi(v);
+#else
+  (void)kind;
+  (void)p;
 #endif
-  if (c == 0) {
-    c = dflt;
-    char name[32];
-    std::snprintf(name, sizeof(name), "HEXBP_SK_%d_%d", kind, p);
-    if (const char* v = std::getenv(name)) c = std::atoi(v);
-  }
-  return c;
+  return dflt;
 }
 
 // z-segments per element column: enough CTAs for `waves` full waves of the

@@ -135,6 +135,12 @@ enum { HEXBP_MODE_REFERENCE = 0, HEXBP_MODE_FAST = 1 };
  *    doubles here (apply never allocates). */
 enum { HEXBP_BACKEND_FUSED = 0, HEXBP_BACKEND_MULTIPASS = 1 };
 int hexbp_workspace_set_backend(hexbp_workspace_t ws, int backend);
+/* Workspace::qpoint_fields / global_bytes (operator.hpp:193-202): the global
+ * quadrature-point fields owned (multipass: 2 x fields, fused: 0) and the
+ * bytes of element-level global scratch (fused: the transpose-restriction
+ * partial buffers, which replace the reference's E-vector; multipass: the
+ * E-vectors and quadrature fields as well). */
+int hexbp_workspace_info(hexbp_workspace_t ws, int* qpoint_fields, uint64_t* global_bytes);
 int hexbp_workspace_set_mode(hexbp_workspace_t ws, int mode);
 
 /* Replaces OperatorHandle::apply(u, w, ws) (operator.hpp:265-279) and, with

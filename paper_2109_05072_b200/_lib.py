@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
         "hexbp_cgd_apply_fused": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
         "hexbp_setup_factors_device": (C.c_int, [_vp, _vp, _vp]),
         "hexbp_uniform_stream": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_int64, _vp]),
+        "hexbp_workspace_info": (C.c_int, [_vp, _vp, _vp]),
         "hexbp_setup_node_coords": (C.c_int, [_vp, _vp, _vp]),
         "hexbp_interp_to_qpts": (C.c_int, [_vp, _vp, _vp, _vp]),
         "hexbp_interp_transpose": (C.c_int, [_vp, _vp, _vp, _vp]),

@@ -301,6 +301,18 @@ class Workspace:
         """'reference' (default): bit-exact reference arithmetic; 'fast': FMA kernels, fused p.Ap."""
         _check(_lib.lib().hexbp_workspace_set_mode(self._h, {"reference": 0, "fast": 1}[mode]))
 
+    def qpoint_fields(self) -> int:
+        """Workspace::qpoint_fields (operator.hpp:193-194)."""
+        q, b = C.c_int(0), C.c_uint64(0)
+        _check(_lib.lib().hexbp_workspace_info(self._h, C.byref(q), C.byref(b)))
+        return q.value
+
+    def global_bytes(self) -> int:
+        """Workspace::global_bytes (operator.hpp:196-201): element-level global scratch."""
+        q, b = C.c_int(0), C.c_uint64(0)
+        _check(_lib.lib().hexbp_workspace_info(self._h, C.byref(q), C.byref(b)))
+        return b.value
+
     def kernel_info(self) -> dict:
         vals = [C.c_int(0) for _ in range(4)]
         _check(_lib.lib().hexbp_kernel_info(self.setup._h, *[C.byref(v) for v in vals]))

@@ -424,8 +424,10 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
     const std::size_t exact = static_cast<std::size_t>(ncols) * 4 * s.p * nz_nodes;
     const std::size_t fast = static_cast<std::size_t>(lat_fast_doubles(s.p, s.dims[0], s.dims[1], nz_nodes));
     al(reinterpret_cast<void**>(&w.lateral), sizeof(double) * (exact > fast ? exact : fast));
+    w.scatter_bytes += sizeof(double) * (exact > fast ? exact : fast);
   }
   al(reinterpret_cast<void**>(&w.zupper), sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * s.dims[2]);
+  w.scatter_bytes += sizeof(double) * static_cast<std::size_t>(ncols) * 4 * s.p * s.dims[2];
   // one partial p.Ap per operator CTA: at most one per (column, z-segment) <= E
   al(reinterpret_cast<void**>(&w.col_dot), sizeof(double) * static_cast<std::size_t>(ncols) * s.dims[2]);
   al(reinterpret_cast<void**>(&w.fix_partials), sizeof(double) * w.fixup_grid);
@@ -779,6 +781,16 @@ int hexbp_workspace_set_backend(hexbp_workspace_t wh, int backend) {
   }
   w.multipass = backend == HEXBP_BACKEND_MULTIPASS;
   if (w.multipass) w.exact = 1;
+  return HEXBP_OK;
+}
+
+int hexbp_workspace_info(hexbp_workspace_t wh, int* qpoint_fields, uint64_t* global_bytes) {
+  if (!wh || !qpoint_fields || !global_bytes) return invalid("null argument");
+  const Workspace& w = wh->w;
+  const int nf = w.s->kind == KIND_MASS ? 1 : 3;
+  *qpoint_fields = w.multipass ? 2 * nf : 0;  // operator.hpp:159-172
+  *global_bytes = w.multipass ? sizeof(double) * static_cast<uint64_t>(multipass_doubles(*w.s)) + w.scatter_bytes
+                              : w.scatter_bytes;
   return HEXBP_OK;
 }
 

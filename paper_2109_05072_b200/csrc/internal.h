@@ -112,6 +112,7 @@ struct Workspace {
   double* dot_result = nullptr;
   DevScalars* host_sc = nullptr;  // pinned mirror
   // host-API solves: b streams in on copy_st while the initial A x0 runs
+  size_t scatter_bytes = 0;  // transpose-restriction scratch (lateral + zupper): Workspace::global_bytes analog
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_x = nullptr, ev_b = nullptr;
 };

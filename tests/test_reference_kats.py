@@ -122,3 +122,22 @@ def test_flop_counter():
     fu = op_for(3, 3, (2, 2, 1), 0.1).count_flops()  # BackendsCountIdenticalElementWork
     mp = op_for(3, 3, (2, 2, 1), 0.1, backend=hx.Backend.CudaMultipass).count_flops()
     assert (fu.mul, fu.add) == (mp.mul, mp.add)
+
+
+def test_multipass_owns_global_quadrature_fields():
+    """test_operator.cpp (Workspace.MultipassOwnsGlobalQuadratureFields): the
+    multipass workspace owns 2 x fields global quadrature fields, the fused
+    one none. The fused path's element-level scratch is the ring-partial
+    buffers that replace the E-vector (~4/p of the nodes plus per-plane
+    corner copies): within one E-vector at p = 7, within two on tiny p = 3
+    meshes."""
+    for dims, p, bound in (((2, 2, 2), 3, 2.0), ((3, 3, 3), 7, 1.0)):
+        mesh = hx.build_box_mesh(dims, p)
+        for bp in (3, 5):
+            setup = hx.make_setup(hx.BPKind(bp), mesh)
+            mp = hx.OperatorHandle(hx.Backend.CudaMultipass, setup).workspace()
+            fu = hx.OperatorHandle(hx.Backend.Cuda, setup).workspace()
+            assert mp.qpoint_fields() >= 3 and fu.qpoint_fields() == 0
+            evec_bytes = setup.num_elements() * (setup.p + 1) ** 3 * 8
+            assert fu.global_bytes() <= bound * evec_bytes, (dims, p, fu.global_bytes(), evec_bytes)
+            assert mp.global_bytes() >= 3 * 8 * setup.num_elements() * setup.q ** 3

@@ -26,7 +26,7 @@
 namespace hexbp::b200 {
 
 enum class BPKind { BP1, BP3, BP5 };
-enum class Backend { Cuda };
+enum class Backend { Cuda, CudaMultipass };  // Backend::Fused / Backend::Multipass on the GPU
 enum class Mode { Reference = HEXBP_MODE_REFERENCE, Fast = HEXBP_MODE_FAST };
 
 class divergence_error : public std::runtime_error {
@@ -111,6 +111,22 @@ class Workspace {  // operator.hpp:148-211
   Workspace(Workspace&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
   Workspace(const Workspace&) = delete;
   void set_mode(Mode m) { check(hexbp_workspace_set_mode(h_, static_cast<int>(m))); }
+  void set_backend(Backend b) {
+    check(hexbp_workspace_set_backend(h_, b == Backend::CudaMultipass ? HEXBP_BACKEND_MULTIPASS
+                                                                      : HEXBP_BACKEND_FUSED));
+  }
+  int qpoint_fields() const {  // operator.hpp:193-194
+    int q = 0;
+    uint64_t b = 0;
+    check(hexbp_workspace_info(h_, &q, &b));
+    return q;
+  }
+  std::size_t global_bytes() const {  // operator.hpp:196-201
+    int q = 0;
+    uint64_t b = 0;
+    check(hexbp_workspace_info(h_, &q, &b));
+    return static_cast<std::size_t>(b);
+  }
   hexbp_workspace_t handle() const { return h_; }
 
  private:
@@ -125,12 +141,17 @@ struct FlopCount {  // tensor.hpp:19-29
 
 class OperatorHandle {
  public:
-  OperatorHandle(Backend, std::shared_ptr<const OperatorSetup> setup)
-      : setup_(std::move(setup)), ws_(std::make_unique<Workspace>(*setup_)) {}
+  OperatorHandle(Backend backend, std::shared_ptr<const OperatorSetup> setup)
+      : backend_(backend), setup_(std::move(setup)), ws_(std::make_unique<Workspace>(make_workspace())) {}
 
   int size() const { return setup_->l_size(); }
   const OperatorSetup& setup() const { return *setup_; }
-  Workspace make_workspace() const { return Workspace(*setup_); }
+  Workspace make_workspace() const {  // operator.hpp:262
+    Workspace w(*setup_);
+    if (backend_ == Backend::CudaMultipass) w.set_backend(backend_);
+    return w;
+  }
+  Backend backend() const { return backend_; }
   Workspace& workspace() const { return *ws_; }
 
   // operator.hpp:265-279 (host vectors; w is resized like the reference's :273)
@@ -163,6 +184,7 @@ class OperatorHandle {
   }
 
  private:
+  Backend backend_ = Backend::Cuda;
   std::shared_ptr<const OperatorSetup> setup_;
   std::unique_ptr<Workspace> ws_;
 };

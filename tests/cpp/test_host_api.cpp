@@ -80,6 +80,17 @@ int main() {
   std::vector<double> x2(b.size(), 0.0);
   const CGReport rf = cg(cop, b, x2, 1e-8, 2000);
   EXPECT(std::abs(rf.iterations - 235) <= 1, "fast mode iterations %d", rf.iterations);
+  // Backend::Multipass analog (the reference's multipass operation order, so
+  // tolerance-level against the fused apply) and the workspace queries of
+  // operator.hpp:193-201
+  const OperatorHandle mp(Backend::CudaMultipass, make_setup(BPKind::BP3, mesh));
+  std::vector<double> wm;
+  mp.apply(u, wm);
+  double dm = 0.0;
+  for (int i = 0; i < op.size(); ++i) dm = std::fmax(dm, std::fabs(wm[i] - w[i]));
+  EXPECT(dm <= 1e-12 * nrm, "multipass vs fused %.3e", dm / nrm);
+  EXPECT(mp.workspace().qpoint_fields() == 6 && op.workspace().qpoint_fields() == 0,
+         "qpoint_fields multipass %d fused %d", mp.workspace().qpoint_fields(), op.workspace().qpoint_fields());
   const FlopCount fc = op.count_flops();
   EXPECT(fc.total() > 0, "count_flops %llu per element", static_cast<unsigned long long>(fc.total()));
   std::printf("%s\n", failures ? "FAILED" : "ALL PASS");

@@ -56,8 +56,14 @@ struct XCfg {
   static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
 };
 
+// CTAs per SM the register allocation targets (measured on a B200: the
+// kernel spills either way at p >= 7; more resident CTAs win for BP3 / BP1
+// at p = 7 and BP1 p = 8, lose for BP3 p = 8; neutral elsewhere)
+constexpr int exact_min_blocks(int p, int kind) {
+  return (p == 7 && kind != KIND_COLLOC) ? 4 : (p == 8 && kind == KIND_MASS) ? 3 : 1;
+}
 template <int P, int Q, int KIND>
-__global__ void __launch_bounds__(XCfg<P, Q, KIND>::NT, 1)
+__global__ void __launch_bounds__(XCfg<P, Q, KIND>::NT, exact_min_blocks(P, KIND))
     bp_apply_exact_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisX<P, Q> bs) {
   using K = XCfg<P, Q, KIND>;
   constexpr int N = K::N, NT = K::NT, QQ = Q * Q;

@@ -190,14 +190,13 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 }
 
 // Work split of the element kernel, per (P, KIND), as a code
-// SK = TPC*1000000 + EO*100000 + G2*10000 + R*100 + S*10 + KC: EO = even-odd contractions
-// (EOB above), G2 = double-buffered G staging, TPC = the thread-per-column
-// kernel below (BP1 p = 1; SK/10 % 100 its min CTAs per SM), S lanes share each pencil (lane s owns quadrature
-// rows s, s+S, ...; the transposed contractions' partial sums are
-// reduce-scattered by warp shuffles), KC element columns share a CTA, and
-// R*8 caps the registers (R = 0: 255). S divides the 2 Q (P+1) basis
-// coefficients a thread keeps in registers; KC fills the warps when Q^2 is
-// small. Values: measured per p on a B200 (profiles/README.md).
+// SK = TPC*1000000 + EO*100000 + R*100 + 10 + KC: KC element columns per CTA
+// (fills the warps when q^2 is small), R*8 a register cap (R = 0: 255), EO the
+// even-odd contractions (EOB above), TPC the thread-per-column kernel below
+// (BP1 p = 1; SK/10 % 100 is then its min CTAs per SM). The tens digit is 1:
+// one lane per pencil (splitting pencils over 2-4 lanes and double-buffered G
+// staging lost every sweep and were removed). Values: measured per p on a B200
+// (profiles/r1c_sk_sweep*.jsonl).
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
   constexpr int mass[9] = {0, 1000000, 16, 100014, 100015, 100013, 100011, 100011, 100011};
@@ -222,15 +221,11 @@ template <int P, int Q, int KIND, int SK>
 struct Cfg {
   static constexpr int N = P + 1;
   static constexpr int QQ = Q * Q;
-  static constexpr bool EO = SK / 100000 % 10;   // even-odd contractions (requires S = 1)
-  static constexpr int GB = SK / 10000 % 10 ? 2 : 1;  // G staging buffers (2: issued one element ahead)
-  static constexpr int S = SK / 10 % 10;  // lanes per pencil (1, 2, 4)
+  static constexpr bool EO = SK / 100000 % 10;   // even-odd contractions
   static constexpr int KC = SK % 10;      // element columns per CTA
   static constexpr int MAXREG = SK / 100 % 100 ? SK / 100 % 100 * 8 : 255;
-  static constexpr int RQ = (Q + S - 1) / S;      // quadrature rows per lane
-  static constexpr int RN = (N + S - 1) / S;      // node outputs per lane (transposed phases)
   static constexpr int ZI = KC * N * N, YI = KC * N * Q, XI = KC * QQ;  // pencils per phase
-  static constexpr int NT = ((S * XI + 31) / 32) * 32;
+  static constexpr int NT = ((XI + 31) / 32) * 32;
   static constexpr int FA = KIND == KIND_MASS ? 1 : 2;  // fields in smem A ([f][c][j][i])
   static constexpr int FB = KIND == KIND_MASS ? 1 : 3;  // fields in smem B ([f][i][c][b])
   static constexpr int SA_CS = best_stride(N, Q, N * N, 0);
@@ -241,60 +236,17 @@ struct Cfg {
   static constexpr int COMP = KIND == KIND_MASS ? 1 : 6;
   static constexpr int GS = (COMP * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
   static constexpr int G_OFF = KC * CB;                      // 16-byte aligned TMA destinations
-  static constexpr int U_OFF = G_OFF + GB * KC * GS;         // per column two u slabs (cp.async double buffer)
+  static constexpr int U_OFF = G_OFF + KC * GS;              // per column two u slabs (cp.async double buffer)
   static constexpr int BAR_OFF = U_OFF + KC * 2 * N * N * N;
-  static constexpr int SMEM_BYTES = (BAR_OFF + GB) * 8;
+  static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
 };
-
-// a[S r + s] for compile-time r and the lane's runtime s (0 past the end)
-template <int S, int L>
-__device__ __forceinline__ double pick(const double (&a)[L], int r, int s) {
-  double v = 0.0;
-#pragma unroll
-  for (int q = 0; q < S; ++q)
-    if (S * r + q < L && s == q) v = a[S * r + q];
-  return v;
-}
-
-// Reduce-scatter over the S lanes of a pencil: lane s receives
-// o[r] = sum over the group's lanes of v[S r + s]. Two-term sums are
-// commutative, so every lane of a pair forms the identical value.
-template <int S, int L, int R>
-__device__ __forceinline__ void reduce_scatter(const double (&v)[L], double (&o)[R], int s) {
-  auto at = [&](int j) -> double { return j < L ? v[j] : 0.0; };
-  if constexpr (S == 1) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) o[r] = at(r);
-  } else if constexpr (S == 2) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double v0 = at(2 * r), v1 = at(2 * r + 1);
-      const double mine = s ? v1 : v0, send = s ? v0 : v1;
-      o[r] = mine + __shfl_xor_sync(0xffffffffu, send, 1);
-    }
-  } else {
-    static_assert(S == 4, "S in {1, 2, 4}");
-    const int b1 = (s >> 1) & 1, b0 = s & 1;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double w[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double lo = at(4 * r + e), hi = at(4 * r + 2 + e);
-        w[e] = (b1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
-      }
-      o[r] = (b0 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, b0 ? w[0] : w[1], 1);
-    }
-  }
-}
 
 template <int P, int Q, int KIND, int SK, typename K_ = Cfg<P, Q, KIND, SK>>
 __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
   using K = Cfg<P, Q, KIND, SK>;
-  constexpr int N = K::N, QQ = K::QQ, NT = K::NT, S = K::S, KC = K::KC, RQ = K::RQ, RN = K::RN;
+  constexpr int N = K::N, QQ = K::QQ, NT = K::NT, KC = K::KC;
   constexpr int NH = N / 2;
-  static_assert(!K::EO || S == 1, "even-odd contractions need one lane per pencil");
   constexpr bool COLLOC = KIND == KIND_COLLOC;
   constexpr bool MASS = KIND == KIND_MASS;
 
@@ -304,9 +256,8 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;  // CG already stopped
 
   const int t = threadIdx.x;
-  const int s = t % S;     // lane within the pencil group
-  const int item = t / S;  // pencil index (per phase)
-  const int wfirst = (t & ~31) / S;  // first pencil of this warp: whole-warp phase skips
+  const int item = t;               // pencil index (per phase)
+  const int wfirst = t & ~31;       // first pencil of this warp: whole-warp phase skips
   const uint64_t pol = policy_evict_first();
   const bool do_dot = A.col_dot != nullptr;
   // CTA = (column group, z-segment). A segment recomputes the element below
@@ -320,13 +271,13 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   const int z_hi = static_cast<int>(static_cast<long long>(seg + 1) * A.nz / nseg);
   const int e0 = seg > 0 ? z_lo - 1 : z_lo;
 
-  // basis rows of this lane: cB[r][i] = B(S r + s, i), cD likewise (0 past Q)
-  double cB[RQ][N], cD[RQ][N];
+  // the basis (plain contractions): cB[a][i] = B(a, i), cD likewise
+  double cB[Q][N], cD[Q][N];
 #pragma unroll
-  for (int r = 0; r < RQ; ++r)
+  for (int r = 0; r < Q; ++r)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const int c = S * r + (S == 1 ? 0 : s);
+      const int c = r;
       cB[r][i] = c < Q ? bs.B[c][i] : 0.0;
       cD[r][i] = c < Q ? bs.D[c][i] : 0.0;
     }
@@ -361,18 +312,16 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   const double* Gcta = A.G + static_cast<long long>(col0) * gcol;
   if (t == 0) {
     mbar_init(bar, 1);
-    if constexpr (K::GB == 2) mbar_init(bar + 8, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue_g = [&](int ez, int buf) {  // thread 0
-    const uint32_t b = bar + 8 * buf;
-    mbar_arrive_expect_tx(b, gbytes * kv);
+  auto issue_g = [&](int ez) {  // thread 0
+    mbar_arrive_expect_tx(bar, gbytes * kv);
     for (int kk = 0; kk < kv; ++kk)
-      bulk_g2s(smem_u32(smem + K::G_OFF + (buf * KC + kk) * K::GS), Gcta + kk * gcol + ez * K::GS, gbytes, b, pol);
+      bulk_g2s(smem_u32(smem + K::G_OFF + kk * K::GS), Gcta + kk * gcol + ez * K::GS, gbytes, bar, pol);
   };
   if (t == 0) {
-    issue_g(e0, 0);
+    issue_g(e0);
     if (e0 + 1 < z_hi)
       for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + (e0 + 1) * K::GS, gbytes);
   }
@@ -380,8 +329,8 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   auto fetch_u = [&](int ez, int buf) {
     if (zvalid) {
 #pragma unroll
-      for (int r = 0; r < RN; ++r) {
-        const int k = S * r + s;
+      for (int r = 0; r < N; ++r) {
+        const int k = r;
         if (k < N) {
           const long long node =
               X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * (ez * P + k));
@@ -402,14 +351,6 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
-    }
-    if constexpr (S > 1) __syncthreads();  // the lanes of a pencil fetched its nodes in turn
-    // two G buffers: element le+1's blocks stream while this element computes
-    // (its buffer was last read by phase X of element le-1, before the
-    // previous iteration's final barrier)
-    if (K::GB == 2 && t == 0 && ez + 1 < z_hi) {
-      fence_proxy_async();
-      issue_g(ez + 1, (le + 1) & 1);
     }
 
     // ---------------- phase Z: gather the z-pencil, contract along z
@@ -442,11 +383,11 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           });
       } else
 #pragma unroll
-      for (int r = 0; r < RQ; ++r) {
-        const int c = S * r + s;
+      for (int r = 0; r < Q; ++r) {
+        const int c = r;
         double s0, s1 = 0.0;
         if constexpr (COLLOC) {
-          s0 = pick<S>(uk, r, s);
+          s0 = uk[r];
         } else {
           s0 = 0.0;
 #pragma unroll
@@ -507,12 +448,12 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           });
       } else
 #pragma unroll
-      for (int r = 0; r < RQ; ++r) {
-        const int b = S * r + s;
+      for (int r = 0; r < Q; ++r) {
+        const int b = r;
         double bb = 0.0, db = 0.0, bd = 0.0;
         if constexpr (COLLOC) {
-          bb = pick<S>(y0, r, s);
-          bd = pick<S>(y1, r, s);
+          bb = y0[r];
+          bd = y1[r];
         } else {
 #pragma unroll
           for (int j = 0; j < N; ++j) bb = fma(cB[r][j], y0[j], bb);
@@ -537,14 +478,13 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     __syncthreads();
 
     // ---------------- phase X: x-pencils, pointwise factors, back along x
-    const int gbuf = K::GB == 2 ? (le & 1) : 0;
-    mbar_wait_parity(bar + 8 * gbuf, K::GB == 2 ? (le >> 1) & 1 : le & 1);  // the G blocks have landed
+    mbar_wait_parity(bar, le & 1);  // the G blocks have landed in shared memory
     if (wfirst < K::XI) {
       const bool act = item < K::XI;
       const int it = act ? item : K::XI - 1;
       const int kx = it / QQ, pp = it % QQ;
       double* SB = smem + kx * K::CB + K::SA_SIZE;
-      const double* Ge = smem + K::G_OFF + (gbuf * KC + kx) * K::GS;
+      const double* Ge = smem + K::G_OFF + kx * K::GS;
       if constexpr (MASS && K::EO) {
         double x0[N], v[Q], out[N];
 #pragma unroll
@@ -557,31 +497,30 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         for (int i = 0; i < N; ++i)
           if (act) SB[i * K::SB_IS + pp] = out[i];
       } else if constexpr (MASS) {
-        double x0[N], v[RQ];
+        double x0[N], v[Q];
 #pragma unroll
         for (int i = 0; i < N; ++i) x0[i] = SB[i * K::SB_IS + pp];
 #pragma unroll
-        for (int r = 0; r < RQ; ++r) {
-          const int a = S * r + s;
+        for (int r = 0; r < Q; ++r) {
+          const int a = r;
           double acc = 0.0;
 #pragma unroll
           for (int i = 0; i < N; ++i) acc = fma(cB[r][i], x0[i], acc);
           v[r] = a < Q ? acc * Ge[a * QQ + pp] : 0.0;
         }
-        double part[N], o[RN];
+        double o[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           double acc = 0.0;
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) acc = fma(cB[r][i], v[r], acc);
-          part[i] = acc;
+          for (int r = 0; r < Q; ++r) acc = fma(cB[r][i], v[r], acc);
+          o[i] = acc;
         }
-        reduce_scatter<S>(part, o, s);
 #pragma unroll
-        for (int r = 0; r < RN; ++r)
-          if (act && S * r + s < N) SB[(S * r + s) * K::SB_IS + pp] = o[r];
+        for (int r = 0; r < N; ++r)
+          if (act && r < N) SB[(r) * K::SB_IS + pp] = o[r];
       } else {
-        double gr[RQ], gs[RQ], gt[RQ];
+        double gr[Q], gs[Q], gt[Q];
         if constexpr (K::EO) {
           double x0[N], x1[N], x2[N];
 #pragma unroll
@@ -614,14 +553,14 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
             x2[i] = SB[(2 * N + i) * K::SB_IS + pp];
           }
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) {
+          for (int r = 0; r < Q; ++r) {
             double rr = 0.0;
 #pragma unroll
             for (int i = 0; i < N; ++i) rr = fma(cD[r][i], x0[i], rr);
             gr[r] = rr;
             if constexpr (COLLOC) {
-              gs[r] = pick<S>(x1, r, s);
-              gt[r] = pick<S>(x2, r, s);
+              gs[r] = x1[r];
+              gt[r] = x2[r];
             } else {
               double ss = 0.0, uu = 0.0;
 #pragma unroll
@@ -635,14 +574,14 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           }
         }
 #pragma unroll
-        for (int r = 0; r < RQ; ++r) {
-          const int a = S * r + s;
+        for (int r = 0; r < Q; ++r) {
+          const int a = r;
           const int ac = a < Q ? a : Q - 1;
           const double* g = Ge + ac * QQ + pp;
           const double g0 = g[0 * Q * QQ], g1 = g[1 * Q * QQ], g2 = g[2 * Q * QQ];
           const double g3 = g[3 * Q * QQ], g4 = g[4 * Q * QQ], g5 = g[5 * Q * QQ];
           const double rr = gr[r], ss = gs[r], uu = gt[r];
-          const bool ok = S == 1 || a < Q;
+          const bool ok = true;
           gr[r] = ok ? g0 * rr + g1 * ss + g2 * uu : 0.0;  // operator.hpp:129-131
           gs[r] = ok ? g1 * rr + g3 * ss + g4 * uu : 0.0;
           gt[r] = ok ? g2 * rr + g4 * ss + g5 * uu : 0.0;
@@ -650,7 +589,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         // back along x, field by field (partials reduce-scattered over the pencil's lanes)
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
-          double part[N], o[RN];
+          double part[N];
           if constexpr (K::EO) {
             if (f == 0) {
               eo_bwd<-1, false>(bs.eD, gr, part);
@@ -669,26 +608,26 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
             double acc = 0.0;
             if (f == 0) {
 #pragma unroll
-              for (int r = 0; r < RQ; ++r) acc = fma(cD[r][i], gr[r], acc);
+              for (int r = 0; r < Q; ++r) acc = fma(cD[r][i], gr[r], acc);
             } else if constexpr (COLLOC) {
-              acc = (S == 1 || s == i % S) ? (f == 1 ? gs[i / S] : gt[i / S]) : 0.0;
+              acc = f == 1 ? gs[i] : gt[i];
             } else {
 #pragma unroll
-              for (int r = 0; r < RQ; ++r) acc = fma(cB[r][i], f == 1 ? gs[r] : gt[r], acc);
+              for (int r = 0; r < Q; ++r) acc = fma(cB[r][i], f == 1 ? gs[r] : gt[r], acc);
             }
             part[i] = acc;
           }
-          reduce_scatter<S>(part, o, s);
+          const double (&o)[N] = part;
 #pragma unroll
-          for (int r = 0; r < RN; ++r)
-            if (act && S * r + s < N) SB[(f * N + S * r + s) * K::SB_IS + pp] = o[r];
+          for (int r = 0; r < N; ++r)
+            if (act && r < N) SB[(f * N + r) * K::SB_IS + pp] = o[r];
         }
       }
     }
     __syncthreads();
-    if (K::GB == 1 && t == 0 && ez + 1 < z_hi) {  // G buffers consumed: stream the next element's blocks
+    if (t == 0 && ez + 1 < z_hi) {  // G buffers consumed: stream the next element's blocks
       fence_proxy_async();
-      issue_g(ez + 1, 0);
+      issue_g(ez + 1);
     }
 
     // ---------------- phase Y': back along y
@@ -699,10 +638,10 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       const int i = rem % N, c = rem / N;
       double* SA = smem + ky * K::CB;
       const double* sb = smem + ky * K::CB + K::SA_SIZE + i * K::SB_IS + c * Q;
-      double a0[RQ], a1[RQ], a2[RQ];
+      double a0[Q], a1[Q], a2[Q];
 #pragma unroll
-      for (int r = 0; r < RQ; ++r) {
-        const int b = S * r + s;
+      for (int r = 0; r < Q; ++r) {
+        const int b = r;
         const int bc = b < Q ? b : Q - 1;  // past-the-end rows carry zero coefficients
         a0[r] = sb[bc];
         if constexpr (!MASS) {
@@ -710,7 +649,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           a2[r] = sb[2 * N * K::SB_IS + bc];
         }
       }
-      double p1[N], p2[N], o1[RN], o2[RN];
+      double p1[N], p2[N];
       if constexpr (K::EO) {
         if constexpr (MASS) {
           eo_bwd<1, false>(bs.eB, a0, p1);
@@ -730,32 +669,32 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double c1 = 0.0, c2 = 0.0;
-        const bool mine = S == 1 || s == j % S;
+        const bool mine = true;
         if constexpr (MASS) {
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) c1 = fma(cB[r][j], a0[r], c1);
+          for (int r = 0; r < Q; ++r) c1 = fma(cB[r][j], a0[r], c1);
         } else if constexpr (COLLOC) {
-          c1 = mine ? a0[j / S] : 0.0;
+          c1 = mine ? a0[j] : 0.0;
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) c1 = fma(cD[r][j], a1[r], c1);
-          c2 = mine ? a2[j / S] : 0.0;
+          for (int r = 0; r < Q; ++r) c1 = fma(cD[r][j], a1[r], c1);
+          c2 = mine ? a2[j] : 0.0;
         } else {
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) {
+          for (int r = 0; r < Q; ++r) {
             c1 = fma(cB[r][j], a0[r], c1);
             c2 = fma(cB[r][j], a2[r], c2);
           }
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) c1 = fma(cD[r][j], a1[r], c1);
+          for (int r = 0; r < Q; ++r) c1 = fma(cD[r][j], a1[r], c1);
         }
         p1[j] = c1;
         p2[j] = c2;
       }
-      reduce_scatter<S>(p1, o1, s);
-      if constexpr (!MASS) reduce_scatter<S>(p2, o2, s);
+      const double (&o1)[N] = p1;
+      const double (&o2)[N] = p2;
 #pragma unroll
-      for (int r = 0; r < RN; ++r) {
-        const int j = S * r + s;
+      for (int r = 0; r < N; ++r) {
+        const int j = r;
         if (act && j < N) {
           SA[c * K::SA_CS + j * N + i] = o1[r];
           if constexpr (!MASS) SA[(Q + c) * K::SA_CS + j * N + i] = o2[r];
@@ -767,15 +706,15 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     // ---------------- phase Z': back along z into the z-pencil
     if (wfirst < K::ZI) {
       const double* SA = smem + kz * K::CB;
-      double c1[RQ], c2[RQ];
+      double c1[Q], c2[Q];
 #pragma unroll
-      for (int r = 0; r < RQ; ++r) {
-        const int c = S * r + s;
+      for (int r = 0; r < Q; ++r) {
+        const int c = r;
         const int cc = c < Q ? c : Q - 1;
         c1[r] = SA[cc * K::SA_CS + pz];
         if constexpr (!MASS) c2[r] = SA[(Q + cc) * K::SA_CS + pz];
       }
-      double part[N], out[RN];
+      double part[N];
       if constexpr (K::EO) {
         if constexpr (COLLOC) {
 #pragma unroll
@@ -789,31 +728,29 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       for (int k = 0; k < N; ++k) {
         double acc = 0.0;
         if constexpr (COLLOC) {
-          acc = (S == 1 || s == k % S) ? c1[k / S] : 0.0;
+          acc = c1[k];
         } else {
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) acc = fma(cB[r][k], c1[r], acc);
+          for (int r = 0; r < Q; ++r) acc = fma(cB[r][k], c1[r], acc);
         }
         if constexpr (!MASS) {
 #pragma unroll
-          for (int r = 0; r < RQ; ++r) acc = fma(cD[r][k], c2[r], acc);
+          for (int r = 0; r < Q; ++r) acc = fma(cD[r][k], c2[r], acc);
         }
         part[k] = acc;
       }
-      reduce_scatter<S>(part, out, s);
+      double (&out)[N] = part;
 
       // ---------------- transpose restriction, part 1 (see header)
-      if (s == 0) out[0] += carry;  // node k = 0 belongs to lane 0
-      // the top plane's value is the next element's carry (lane P % S -> lane 0)
-      const double top = out[P / S];
-      carry = S == 1 ? top : __shfl_sync(0xffffffffu, top, (t & 31) - s + P % S);
+      out[0] += carry;
+      carry = out[P];  // the top plane is the next element's bottom plane
       const int kend = (ez == A.nz - 1) ? N : P;
       const double* usz = Uz + (le & 1) * N * N * N;  // u of this element, still staged
       if (zvalid && ez >= z_lo) {
         if (!do_dot) {  // plain apply: the lean epilogue
 #pragma unroll
-          for (int r = 0; r < RN; ++r) {
-            const int k = S * r + s;
+          for (int r = 0; r < N; ++r) {
+            const int k = r;
             if (k < kend) {
               const int Z = ez * P + k;
               if (ring) {
@@ -829,8 +766,8 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           }
         } else {
 #pragma unroll
-          for (int r = 0; r < RN; ++r) {
-            const int k = S * r + s;
+          for (int r = 0; r < N; ++r) {
+            const int k = r;
             if (k < kend) {
               const int Z = ez * P + k;
               const double uv = usz[k * N * N];

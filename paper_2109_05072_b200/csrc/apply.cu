@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
         }
 #pragma unroll
         for (int r = 0; r < N; ++r)
-          if (act && r < N) SB[(r) * K::SB_IS + pp] = o[r];
+          if (act) SB[r * K::SB_IS + pp] = o[r];
       } else {
         double gr[Q], gs[Q], gt[Q];
         if constexpr (K::EO) {
@@ -581,10 +581,9 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           const double g0 = g[0 * Q * QQ], g1 = g[1 * Q * QQ], g2 = g[2 * Q * QQ];
           const double g3 = g[3 * Q * QQ], g4 = g[4 * Q * QQ], g5 = g[5 * Q * QQ];
           const double rr = gr[r], ss = gs[r], uu = gt[r];
-          const bool ok = true;
-          gr[r] = ok ? g0 * rr + g1 * ss + g2 * uu : 0.0;  // operator.hpp:129-131
-          gs[r] = ok ? g1 * rr + g3 * ss + g4 * uu : 0.0;
-          gt[r] = ok ? g2 * rr + g4 * ss + g5 * uu : 0.0;
+          gr[r] = g0 * rr + g1 * ss + g2 * uu;  // operator.hpp:129-131
+          gs[r] = g1 * rr + g3 * ss + g4 * uu;
+          gt[r] = g2 * rr + g4 * ss + g5 * uu;
         }
         // back along x, field by field (partials reduce-scattered over the pencil's lanes)
 #pragma unroll
@@ -620,7 +619,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
           const double (&o)[N] = part;
 #pragma unroll
           for (int r = 0; r < N; ++r)
-            if (act && r < N) SB[(f * N + r) * K::SB_IS + pp] = o[r];
+            if (act) SB[(f * N + r) * K::SB_IS + pp] = o[r];
         }
       }
     }
@@ -669,15 +668,14 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double c1 = 0.0, c2 = 0.0;
-        const bool mine = true;
         if constexpr (MASS) {
 #pragma unroll
           for (int r = 0; r < Q; ++r) c1 = fma(cB[r][j], a0[r], c1);
         } else if constexpr (COLLOC) {
-          c1 = mine ? a0[j] : 0.0;
+          c1 = a0[j];
 #pragma unroll
           for (int r = 0; r < Q; ++r) c1 = fma(cD[r][j], a1[r], c1);
-          c2 = mine ? a2[j] : 0.0;
+          c2 = a2[j];
         } else {
 #pragma unroll
           for (int r = 0; r < Q; ++r) {

@@ -122,8 +122,12 @@ void hexbp_workspace_destroy(hexbp_workspace_t ws);
  *    fused into the operator kernel, FMA updates, fixed-order tree
  *    reductions: operator within ~3e-16 of the reference per entry, bitwise
  *    reproducible run to run, iterates equal to the reference's up to
- *    rounding. hexbp_dot always uses the reference order. */
-enum { HEXBP_MODE_REFERENCE = 0, HEXBP_MODE_FAST = 1 };
+ *    rounding. hexbp_dot always uses the reference order.
+ *  HEXBP_MODE_FAST_OPERATOR: the fast operator kernel under the reference's
+ *    CG recurrence -- deterministic_dot-order inner products and the
+ *    unfused vector updates of REFERENCE mode -- so a solve differs from the
+ *    reference only by the operator's rounding (the parity-diagnosis mode). */
+enum { HEXBP_MODE_REFERENCE = 0, HEXBP_MODE_FAST = 1, HEXBP_MODE_FAST_OPERATOR = 2 };
 
 /* Operator backend of a workspace (Backend, operator.hpp:31):
  *  HEXBP_BACKEND_FUSED (default): one fused kernel per apply (Backend::Fused).

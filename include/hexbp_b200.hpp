@@ -27,7 +27,7 @@ namespace hexbp::b200 {
 
 enum class BPKind { BP1, BP3, BP5 };
 enum class Backend { Cuda, CudaMultipass };  // Backend::Fused / Backend::Multipass on the GPU
-enum class Mode { Reference = HEXBP_MODE_REFERENCE, Fast = HEXBP_MODE_FAST };
+enum class Mode { Reference = HEXBP_MODE_REFERENCE, Fast = HEXBP_MODE_FAST, FastOperator = HEXBP_MODE_FAST_OPERATOR };
 
 class divergence_error : public std::runtime_error {
  public:

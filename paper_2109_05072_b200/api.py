@@ -292,14 +292,19 @@ class Workspace:
 
     def dot(self, a, b) -> float:
         """deterministic_dot (dense.hpp:74-81) of two device tensors."""
+        n = a.numel()
+        _check_device_vec(a, n, "dot")
+        _check_device_vec(b, n, "dot")
         out = C.c_double(0.0)
-        _check(_lib.lib().hexbp_dot(self._h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), a.numel(),
+        _check(_lib.lib().hexbp_dot(self._h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), n,
                                     C.byref(out), _stream_ptr(a)))
         return out.value
 
     def set_mode(self, mode: str) -> None:
-        """'reference' (default): bit-exact reference arithmetic; 'fast': FMA kernels, fused p.Ap."""
-        _check(_lib.lib().hexbp_workspace_set_mode(self._h, {"reference": 0, "fast": 1}[mode]))
+        """'reference' (default): bit-exact reference arithmetic; 'fast': FMA / DMMA kernels, fused p.Ap;
+        'fast_operator': the fast operator kernel under the reference's CG recurrence and
+        deterministic_dot order (only the operator's rounding differs from the reference)."""
+        _check(_lib.lib().hexbp_workspace_set_mode(self._h, {"reference": 0, "fast": 1, "fast_operator": 2}[mode]))
 
     def qpoint_fields(self) -> int:
         """Workspace::qpoint_fields (operator.hpp:193-194)."""
@@ -346,7 +351,7 @@ def _check_device_vec(t, n: int, name: str):
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError(f"{name}: expected a contiguous float64 CUDA tensor")
     if t.numel() != n:
-        raise ValueError("apply: L-vector length mismatch")
+        raise ValueError(f"{name}: L-vector length mismatch")
 
 
 class OperatorHandle:
@@ -399,11 +404,17 @@ class OperatorHandle:
         u = np.ascontiguousarray(u, np.float64)
         if u.size != n:
             raise ValueError("apply: L-vector length mismatch")  # operator.hpp:268
-        out = np.empty(n) if w is None or not isinstance(w, np.ndarray) or w.size != n else w
+        # write through the caller's w only when it is a contiguous float64 array of
+        # length n; otherwise apply into a fresh array (the reference resizes w,
+        # operator.hpp:273) and copy into w where its shape allows
+        direct = isinstance(w, np.ndarray) and w.dtype == np.float64 and w.size == n and w.flags.c_contiguous
+        out = w if direct else np.empty(n)
         _check(_lib.lib().hexbp_apply_host(self._setup._h, ws._h, u.ctypes.data_as(_dp), out.ctypes.data_as(_dp), n,
                                            constrained))
         if isinstance(w, list):
             w[:] = out.tolist()
+        elif isinstance(w, np.ndarray) and not direct and w.size == n:
+            w[...] = out.reshape(w.shape)
         return out
 
     def apply(self, u, w=None, ws: Optional[Workspace] = None, flops: Optional[FlopCount] = None):
@@ -489,6 +500,9 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
         _check_device_vec(b, n, "cg")
         if not _is_torch(x) or x.numel() != n:
             raise ValueError("cg: x0 length mismatch")
+        _check_device_vec(x, n, "cg")
+        if x.device != b.device:
+            raise ValueError("cg: x and b on different devices")
         dptr = None
         if diag is not None:  # Jacobi preconditioner (solver.hpp:105-108)
             import torch

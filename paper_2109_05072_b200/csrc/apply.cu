@@ -1019,12 +1019,9 @@ __global__ void __launch_bounds__(FT) lateral_fixup_kernel(const __grid_constant
 
 template <int P, int Q, int KIND, int SK>
 void* kernel_ptr() {
-  static bool configured = false;  // opt in to > 48 KB dynamic shared memory once per instantiation
-  if (!configured) {
-    cudaFuncSetAttribute(&bp_apply_kernel<P, Q, KIND, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<P, Q, KIND, SK>::SMEM_BYTES);
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // > 48 KB dynamic shared memory, per device
+  set_smem_attr_once(configured, reinterpret_cast<const void*>(&bp_apply_kernel<P, Q, KIND, SK>),
+                     Cfg<P, Q, KIND, SK>::SMEM_BYTES);
   return reinterpret_cast<void*>(&bp_apply_kernel<P, Q, KIND, SK>);
 }
 
@@ -1276,7 +1273,7 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
     if (dot_out || sc) return cudaErrorInvalidValue;
     return launch_apply_multipass(s, ws.mp_buf, u, w, constrained, st);
   }
-  if (ws.exact) {
+  if (ws.exact && !ws.fast_op) {
     if (dot_out || sc) return cudaErrorInvalidValue;  // the exact path reduces in cg.cu
     return launch_apply_exact(s, a, ws.fixup_grid, st);
   }

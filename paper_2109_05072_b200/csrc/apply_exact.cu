@@ -503,12 +503,8 @@ __global__ void __launch_bounds__(FT) lateral_fixup_exact_kernel(const __grid_co
 template <int P, int Q, int KIND>
 cudaError_t launch_x(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   using K = XCfg<P, Q, KIND>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(&bp_apply_exact_kernel<P, Q, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         K::SMEM_BYTES);
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  set_smem_attr_once(configured, reinterpret_cast<const void*>(&bp_apply_exact_kernel<P, Q, KIND>), K::SMEM_BYTES);
   if (s.gstride != K::GS) return cudaErrorInvalidValue;
   BasisX<P, Q> bs;
   for (int i = 0; i < Q; ++i)

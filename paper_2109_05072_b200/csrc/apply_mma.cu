@@ -43,8 +43,11 @@ namespace hxb {
 namespace {
 
 constexpr int P = 7, N = 8, Q = 9, QQ = 81;
-// 11 warps: phase X (the heaviest, 11 pencil groups) runs one group per warp.
-constexpr int NW = 11, NT = NW * 32;
+// Phase X (the heaviest, 11 pencil groups) runs one group per warp on warps
+// 0..10; a 12th warp takes five of the eight Z items of interval A off them
+// (12 warps x 80 registers still fit two CTAs per SM).
+constexpr int NXW = 11;
+constexpr int NW = 12, NT = NW * 32;
 constexpr int GSE = (6 * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
 // shared-memory layout (doubles)
 constexpr int US_KS = 68;                 // u staging: [k][j*8+i], k-stride 68
@@ -285,10 +288,13 @@ __global__ void __launch_bounds__(NT, 2)
     double r8s = quad_sum(row8B(x10, x11));
     double r8t = quad_sum(row8B(x20, x21));
     const int p = 8 * G + g;
-    if (p < QQ) {
+    {
       // pointwise factors (operator.hpp:129-131); [qp][6] layout, qp = a + 9p:
-      // points a = 2t, 2t+1 are 12 contiguous doubles (conflict-free 16-byte loads)
-      const double2* gp = reinterpret_cast<const double2*>(Gs + (2 * t + Q * p) * 6);
+      // points a = 2t, 2t+1 are 12 contiguous doubles (conflict-free 16-byte loads).
+      // Pencils p >= 81 of the last group read pencil 80's factors (their
+      // results are never stored), which keeps the phase branch-free.
+      const int pc = p < QQ ? p : QQ - 1;
+      const double2* gp = reinterpret_cast<const double2*>(Gs + (2 * t + Q * pc) * 6);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const double2 ga = gp[3 * e], gb = gp[3 * e + 1], gc = gp[3 * e + 2];
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(NT, 2)
         gs[e] = ga.y * r + gb.y * s_ + gc.x * u;
         gt[e] = gb.x * r + gc.x * s_ + gc.y * u;
       }
-      const double2* g8 = reinterpret_cast<const double2*>(Gs + (8 + Q * p) * 6);
+      const double2* g8 = reinterpret_cast<const double2*>(Gs + (8 + Q * pc) * 6);
       const double2 ga = g8[0], gb = g8[1], gc = g8[2];
       const double r = r8r, s_ = r8s, u = r8t;
       r8r = ga.x * r + ga.y * s_ + gb.x * u;
@@ -362,14 +368,13 @@ __global__ void __launch_bounds__(NT, 2)
   // (this warp always owns group j).
   double carry[2] = {0.0, 0.0};
   double dot = 0.0;
-  auto phaseZp = [&](int e, int G) {
+  auto phaseZpMath = [&](int G, double* o) {
     const double* sc = SC + 8 * G + g;
     const double z00 = sc[t * SC_KS], z01 = sc[(t + 4) * SC_KS];
     const double z10 = sc[SC_F + t * SC_KS], z11 = sc[SC_F + (t + 4) * SC_KS];
     const double* s8 = SC + 8 * SC_KS + 8 * G + 2 * t;  // c = 8
     const double2 e1 = *reinterpret_cast<const double2*>(s8);
     const double2 e2 = *reinterpret_cast<const double2*>(s8 + SC_F);
-    double o[2];
     const double2 bd8 = c8();
     o[0] = fma(bd8.y, e2.x, bd8.x * e1.x);
     o[1] = fma(bd8.y, e2.y, bd8.x * e1.y);
@@ -377,6 +382,8 @@ __global__ void __launch_bounds__(NT, 2)
     dmma(o[0], o[1], tB1, z01);
     dmma(o[0], o[1], tD0, z10);
     dmma(o[0], o[1], tD1, z11);
+  };
+  auto phaseZpStore = [&](int e, int G, double* o) {
     // rows k = g (z node), cols i = 2t, 2t+1, j = G
     const double top0 = __shfl_sync(0xffffffffu, carry[0], 28 + t);
     const double top1 = __shfl_sync(0xffffffffu, carry[1], 28 + t);
@@ -423,6 +430,12 @@ __global__ void __launch_bounds__(NT, 2)
     }
   };
 
+  auto phaseZp = [&](int e, int G) {
+    double o[2];
+    phaseZpMath(G, o);
+    phaseZpStore(e, G, o);
+  };
+
   // ------------------------------------------------ skewed schedule
   // Two barrier intervals per element, each mixing independent work of
   // neighbouring elements so that no warp idles through a phase:
@@ -433,8 +446,9 @@ __global__ void __launch_bounds__(NT, 2)
   // during B_e (TMA, mbarrier); u of element e+2 is staged (cp.async) during
   // A_e and B_e into one of NUB = 4 buffers (Z'(e-1) still reads u(e-1) for
   // the p.Ap dot).
-  // Work map: Z'(j) on warp j (its carry registers), Z(j) on warp (j+8) % 11,
-  // Y'(c) on warp c, Y(c) on warp (c+9) % 11.
+  // Work map: Z'(j) on warp j (its carry registers), Z(0..4) on warp 11 and
+  // Z(5..7) on warps 8..10, X(G) on warp G < 11, Y'(c) on warp c, Y(c) on
+  // warp (c+9) % 12.
   fetch_u(0);
   fetch_u(1);
   cp_async_wait<0>();
@@ -447,14 +461,20 @@ __global__ void __launch_bounds__(NT, 2)
     // ---- interval A_e
     fetch_u(e + 2);
     if (tid == 0 && e + 2 < nz) prefetch_l2_bulk(Gcol + (e + 2) * GSE, gbytes);
-    if (e < nz) {
-      mbar_wait_parity(bar, e & 1);
-      phaseX(warp);
-    }
+    // Z'(e-1) and Z(e+1) first: they do not read G, so the G(e) transfer
+    // issued in B_{e-1} has the longest time to land before X(e) waits on it
     if (e >= 1 && warp < N) phaseZp(e - 1, warp);
     if (e + 1 < nz) {
-      const int j = warp >= 8 ? warp - 8 : warp + 3;  // inverse of (j + 8) % 11
-      if (j < N) phaseZ(e + 1, j);
+      // warp 11: Z(0..4); warps 8..10: Z(5..7) beside their X group
+      if (warp == NXW) {
+        for (int j = 0; j < 5; ++j) phaseZ(e + 1, j);
+      } else if (warp >= 8) {
+        phaseZ(e + 1, warp - 3);
+      }
+    }
+    if (e < nz && warp < NXW) {
+      mbar_wait_parity(bar, e & 1);
+      phaseX(warp);
     }
     if (e == nz) break;
     __syncthreads();
@@ -466,7 +486,8 @@ __global__ void __launch_bounds__(NT, 2)
     }
     if (warp < Q) phaseYp(warp);
     if (e + 1 < nz) {
-      const int c = warp >= 9 ? warp - 9 : warp + 2;  // inverse of (c + 9) % 11
+      // Y(c) on warp (c + 9) % NW
+      const int c = warp >= 9 ? warp - 9 : warp + NW - 9;
       if (c < Q) phaseY(c);
     }
     cp_async_wait<0>();  // u(e+2), issued at the top of A_e, is read by Z(e+2) in A_{e+1}
@@ -493,11 +514,8 @@ __global__ void __launch_bounds__(NT, 2)
 bool mma_kernel_applies(const Setup& s) { return s.kind == KIND_DIFF && s.p == P && s.gstride == GSE; }
 
 cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(&bp3_p7_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  set_smem_attr_once(configured, reinterpret_cast<const void*>(&bp3_p7_mma_kernel), SMEM_BYTES);
   MmaBasis bs;
   for (int i = 0; i < Q; ++i)
     for (int j = 0; j < N; ++j) {

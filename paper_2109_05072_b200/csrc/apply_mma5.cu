@@ -287,11 +287,8 @@ __global__ void __launch_bounds__(NT, 3)
 bool mma5_kernel_applies(const Setup& s) { return s.kind == KIND_COLLOC && s.p == P && s.g_aos == 2; }
 
 cudaError_t launch_apply_mma5(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(&bp5_p7_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  set_smem_attr_once(configured, reinterpret_cast<const void*>(&bp5_p7_mma_kernel), SMEM_BYTES);
   if (s.gstride != GSE) return cudaErrorInvalidValue;
   Mma5Basis bs;
   for (int i = 0; i < N; ++i)

@@ -478,7 +478,7 @@ int hexbp_apply_ring_deferred(hexbp_setup_t h, hexbp_workspace_t wh, const doubl
   if (!h || !wh || !u || !w) return invalid("apply: null argument");
   if (wh->w.s != &h->s) return invalid("apply: workspace belongs to another setup");
   if (u == w) return invalid("apply: u and w must not alias");
-  if (wh->w.exact) return invalid("apply_ring_deferred: fast-mode workspaces only");
+  if (wh->w.exact && !wh->w.fast_op) return invalid("apply_ring_deferred: fast-mode workspaces only");
   DeviceGuard g(h->s.device);
   CK(launch_apply(h->s, wh->w, u, w, constrained, nullptr, nullptr, static_cast<cudaStream_t>(stream), false));
   return HEXBP_OK;
@@ -655,6 +655,9 @@ int hexbp_cg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double
 int hexbp_dot(hexbp_workspace_t wh, const double* a, const double* b, int64_t n, double* out, void* stream) {
   if (!wh || !a || !b || !out) return invalid("dot: null argument");
   Workspace& w = wh->w;
+  // the chunk partials live in the workspace's vec_partials (sized for the
+  // setup's L-vector at workspace creation)
+  if (n < 0 || n > dot_capacity(w.s->nL)) return invalid("dot: length exceeds the workspace's reduction buffer");
   DeviceGuard g(w.device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* dres = w.dot_result;
@@ -759,10 +762,12 @@ int hexbp_plane_combine(double* dst, const double* src, const double* u, int nxn
 }
 
 int hexbp_workspace_set_mode(hexbp_workspace_t wh, int mode) {
-  if (!wh || (mode != HEXBP_MODE_REFERENCE && mode != HEXBP_MODE_FAST)) return invalid("bad arithmetic mode");
-  if (wh->w.multipass && mode == HEXBP_MODE_FAST)
+  if (!wh || (mode != HEXBP_MODE_REFERENCE && mode != HEXBP_MODE_FAST && mode != HEXBP_MODE_FAST_OPERATOR))
+    return invalid("bad arithmetic mode");
+  if (wh->w.multipass && mode != HEXBP_MODE_REFERENCE)
     return invalid("the multipass backend runs in reference arithmetic only");
-  wh->w.exact = mode == HEXBP_MODE_REFERENCE;
+  wh->w.exact = mode != HEXBP_MODE_FAST;
+  wh->w.fast_op = mode == HEXBP_MODE_FAST_OPERATOR;
   return HEXBP_OK;
 }
 
@@ -780,7 +785,10 @@ int hexbp_workspace_set_backend(hexbp_workspace_t wh, int backend) {
     if (e != cudaSuccess) return cuda_status(e, "multipass basis upload");
   }
   w.multipass = backend == HEXBP_BACKEND_MULTIPASS;
-  if (w.multipass) w.exact = 1;
+  if (w.multipass) {
+    w.exact = 1;
+    w.fast_op = 0;
+  }
   return HEXBP_OK;
 }
 

@@ -668,6 +668,8 @@ int wave_grid(K kernel, int64_t n) {
   return g < cap ? g : cap;
 }
 
+int64_t dot_capacity(int64_t nL) { return reduction_partials(nL) * CHUNK; }
+
 int64_t reduction_partials(int64_t n) {
   // exact-mode chunk partials, or two partials per CTA of the fused kernels
   const int64_t nch = (n + CHUNK - 1) / CHUNK;

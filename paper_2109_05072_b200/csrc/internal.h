@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -17,6 +18,18 @@ namespace hxb {
 //   DIFF   = BP3, q = p+2 Gauss, six factors per point (G)
 //   COLLOC = BP5, q = p+1 GLL (B = I exactly, basis.hpp:55-66), six factors
 enum Kind : int { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
+
+// Opt a kernel in to more than 48 KB of dynamic shared memory. The attribute
+// is per device, so it is set once per (call site, device): `mask` is the call
+// site's bit set of devices already configured.
+inline void set_smem_attr_once(std::atomic<uint64_t>& mask, const void* fn, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  mask.fetch_or(bit, std::memory_order_release);
+}
 
 constexpr int kMaxP = 8;
 constexpr int kMaxQ = kMaxP + 2;
@@ -106,6 +119,7 @@ struct Workspace {
   int history_cap = 0;
   int vec_blocks = 0;
   int exact = 1;                  // reduction mode (cg.cu): 1 = reference order, 0 = fused
+  int fast_op = 0;                // HEXBP_MODE_FAST_OPERATOR: fast operator kernel under the exact CG
   const double* diag = nullptr;   // Jacobi diagonal of the running solve (nullptr: no preconditioner)
   int multipass = 0;              // HEXBP_BACKEND_MULTIPASS (multipass.cu)
   double* mp_buf = nullptr;       // its E-vectors, quadrature fields and basis tables
@@ -162,6 +176,9 @@ cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u,
 // ---- jacobi.cu: jacobi_diagonal (solver.hpp:155-205) in reference arithmetic
 cudaError_t launch_jacobi_diagonal(const Setup& s, int constrained, double* diag, cudaStream_t st);
 int64_t reduction_partials(int64_t n);
+// Longest vector hexbp_dot can reduce with a workspace made for an L-vector of nL
+// entries: one deterministic_dot chunk partial per vec_partials slot.
+int64_t dot_capacity(int64_t nL);
 cudaError_t launch_cgd_reduce(const Workspace& ws, int op, const double* b, int64_t n, int64_t owned, double* out,
                               cudaStream_t st);
 cudaError_t launch_cgd_finish(const Workspace& ws, int op, const double* gathered, int world, double rel_tol,

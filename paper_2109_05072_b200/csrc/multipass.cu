@@ -235,12 +235,9 @@ cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u,
   }
   const size_t smg = sizeof(double) * (2 * q * n + nen + 2 * big * big * big + 3 * q3);
   const size_t smt = sizeof(double) * (2 * q * n + 3 * q3 + nen + 3 * big * big * big);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(&mp_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(&mp_gradT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    configured = true;
-  }
+  static std::atomic<uint64_t> cfg_grad{0}, cfg_gradT{0};
+  set_smem_attr_once(cfg_grad, reinterpret_cast<const void*>(&mp_grad_kernel), 100 * 1024);
+  set_smem_attr_once(cfg_gradT, reinterpret_cast<const void*>(&mp_gradT_kernel), 100 * 1024);
   const int grid = 148 * 8;
   mp_gather_kernel<<<grid, 256, 0, st>>>(c, u, ue, s.E);
   mp_grad_kernel<<<static_cast<unsigned>(s.E), 256, smg, st>>>(c, dB, dD, ue, gq);

@@ -40,7 +40,13 @@ for rep in range(3):
     hx.cg(A, b, x, 0.0, 20, mode="fast")
     ev[1].record(); torch.cuda.synchronize()
     best_cg = min(best_cg, ev[0].elapsed_time(ev[1]) / 20)
-print(json.dumps({"kernel_ms": best_k, "cg_ms_per_it": best_cg, "GDOFps": n / best_cg / 1e6}))
+# correctness of the variant: fast vs reference-mode apply on a multi-wave mesh
+sm = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind.BP3, hx.build_box_mesh((20, 18, 16), p, (1, 1, 1), 0.1)))
+us = torch.empty(sm.size(), dtype=torch.float64, device="cuda").uniform_(-1, 1)
+sm.workspace().set_mode("reference"); wr = hx.ConstrainedOperator(sm).apply(us)
+sm.workspace().set_mode("fast"); wf = hx.ConstrainedOperator(sm).apply(us)
+err = (torch.linalg.norm(wf - wr) / torch.linalg.norm(wr)).item()
+print(json.dumps({"kernel_ms": best_k, "cg_ms_per_it": best_cg, "GDOFps": n / best_cg / 1e6, "rel_err": err}))
 '''
 for lib in sys.argv[1:]:
     env = dict(os.environ, HEXBP_LIB=os.path.abspath(lib))

@@ -26,6 +26,10 @@ raw = list(csv.reader(io.StringIO(run(["--page", "raw", "--csv"]))))
 names, vals = raw[0], raw[2]
 d = dict(zip(names, vals))
 for k in ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+          "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+          "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+          "sm__inst_executed_pipe_tensor_subpipe_dmma.sum", "sm__inst_executed_pipe_fp64.sum",
+          "sm__sass_thread_inst_executed_ops_dadd_dmul_dfma_pred_on.sum",
           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
           "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
           "smsp__inst_executed.sum", "sass__inst_executed_local_loads", "sass__inst_executed_local_stores"]:

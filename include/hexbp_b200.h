@@ -37,6 +37,7 @@ enum {
 
 typedef struct hexbp_setup_s* hexbp_setup_t;         /* device OperatorSetup (operator.hpp:60-68) */
 typedef struct hexbp_workspace_s* hexbp_workspace_t; /* device Workspace (operator.hpp:148-211)   */
+typedef struct hexbp_dist_s* hexbp_dist_t;           /* z-slab operator + CG of one rank (NCCL)  */
 
 typedef struct {
   int bp;            /* 1, 3 or 5 (BPKind, operator.hpp:29) */
@@ -105,10 +106,20 @@ int hexbp_interp_to_qpts(hexbp_setup_t s, const double* v_dev, double* out_dev, 
 int hexbp_interp_transpose(hexbp_setup_t s, const double* vq_dev, double* out_dev, void* stream);
 
 /* Replaces OperatorHandle::make_workspace (operator.hpp:262): ticket/progress
- * flags, per-column partial sums, CG vectors and scalars. All device memory
- * is allocated here; apply and cg never allocate. */
+ * flags, per-column partial sums, CG vectors and scalars, a 4096-iteration CG
+ * history. Device-pointer apply / cg never allocate (cg within the reserved
+ * history); the host-pointer entry points allocate their L-vector staging on
+ * first use unless hexbp_workspace_reserve was called. */
 int hexbp_workspace_create(hexbp_setup_t s, hexbp_workspace_t* out);
 void hexbp_workspace_destroy(hexbp_workspace_t ws);
+/* Optional explicit reservation (Workspace construction, operator.hpp:148-211,
+ * allocates everything up front; test_operator.cpp:184-194): the device CG
+ * history for solves of up to max_iter iterations (4096 are reserved at
+ * creation) and, with host_staging != 0, the two L-vector staging buffers
+ * of the host-pointer entry points (hexbp_apply_host / hexbp_cg_host /
+ * hexbp_pcg_host, which otherwise allocate them on first use). After a
+ * successful reserve, those calls allocate nothing for solves within it. */
+int hexbp_workspace_reserve(hexbp_workspace_t ws, int max_iter, int host_staging);
 
 /* Arithmetic mode of hexbp_apply / hexbp_cg on this workspace:
  *  HEXBP_MODE_REFERENCE (default): bit-exact reference arithmetic. The
@@ -261,6 +272,47 @@ int hexbp_cgd_apply_fused(hexbp_setup_t setup, hexbp_workspace_t ws, int constra
 /* r -= alpha Ap with the ring sums fused (shared planes read from the
  * halo-summed Ap); this rank's r.r over owned nodes -> *partial_dev. */
 int hexbp_cgd_update_r_fused(hexbp_workspace_t ws, int constrained, double* partial_dev, void* stream);
+
+/* ---- Multi-GPU z-slab operator and CG over NCCL (one process per GPU).
+ * The reference's OperatorHandle::apply / cg (operator.hpp:265-279,
+ * solver.hpp:91-153) on a partition of the box into contiguous element
+ * layers per rank (rank order = z order); the library owns the NCCL
+ * communicator. Rank 0 creates the id with hexbp_dist_unique_id and the
+ * caller broadcasts its bytes (MPI, a file, torch.distributed) before every
+ * rank calls hexbp_dist_create[_box]. Per operator apply: the boundary
+ * element layers first, the shared-plane exchange (ncclSend/ncclRecv) while
+ * the interior layers compute on a second stream, then the planes' halo sum
+ * (dst + src on both ranks: bitwise equal copies). CG scalars: rank partials
+ * over owned nodes, ncclAllGather, rank-order sum -- every rank runs the same
+ * recurrence. HEXBP_DIST_NO_OVERLAP: one launch per apply, exchange after. */
+enum { HEXBP_DIST_NO_OVERLAP = 1 };
+int hexbp_dist_unique_id(void* id, int64_t bytes); /* >= 128 bytes (ncclUniqueId) */
+/* Adopt this rank's slab setup (hexbp_setup_create_box_slab: layers [z0, z1)
+ * of the global box); collective over the `world` ranks. */
+int hexbp_dist_create(hexbp_setup_t slab, int world, int rank, const void* id, int64_t id_bytes, int flags,
+                      hexbp_dist_t* out);
+/* Same, building this rank's share of build_box_mesh(gdims, p, extent, amplitude)
+ * (balanced split: rank r gets layers [r*b + min(r, m), ...) with gz = b*world + m). */
+int hexbp_dist_create_box(int bp, int p, const int gdims[3], const double extent[3], double amplitude, int world,
+                          int rank, int device, const void* id, int64_t id_bytes, int flags, hexbp_dist_t* out);
+void hexbp_dist_destroy(hexbp_dist_t d);
+/* This rank's setup, world, rank, local L-vector length, first owned local
+ * index (plane 0 belongs to the rank below) and global index of local node 0. */
+int hexbp_dist_info(hexbp_dist_t d, hexbp_setup_t* setup, int* world, int* rank, int64_t* l_size,
+                    int64_t* owned_offset, int64_t* global_offset);
+/* HEXBP_MODE_FAST (default: the fused iteration) or HEXBP_MODE_REFERENCE
+ * (reference-arithmetic operator, deterministic_dot-order rank partials). */
+int hexbp_dist_set_mode(hexbp_dist_t d, int mode);
+/* w = assembled local part of A u (OperatorHandle::apply on the partition). Collective. */
+int hexbp_dist_apply(hexbp_dist_t d, const double* u_dev, double* w_dev, int constrained, void* stream);
+/* cg (solver.hpp:91-153) on the partition: b, x = this rank's local vectors
+ * (x holds x0); every rank returns the same report. Collective. */
+int hexbp_dist_cg(hexbp_dist_t d, const double* b_dev, double* x_dev, double rel_tol, int max_iter, int constrained,
+                  hexbp_cg_report* report, double* history, void* stream);
+/* The same with HOST vectors (this rank's slices; staged through the workspace). */
+int hexbp_dist_apply_host(hexbp_dist_t d, const double* u, double* w, int64_t n, int constrained);
+int hexbp_dist_cg_host(hexbp_dist_t d, const double* b, double* x, int64_t n, double rel_tol, int max_iter,
+                       int constrained, hexbp_cg_report* report, double* history);
 
 /* Kernel resource report: registers/thread, static+dynamic smem bytes,
  * threads per CTA, resident CTAs per SM. */

@@ -254,6 +254,77 @@ inline std::vector<double> jacobi(const OperatorHandle& op, int constrained) {
 inline std::vector<double> jacobi_diagonal(const OperatorHandle& op) { return detail::jacobi(op, 0); }
 inline std::vector<double> jacobi_diagonal(const ConstrainedOperator& op) { return detail::jacobi(op.raw(), 1); }
 
+// ---- Multi-GPU: the z-slab operator and CG of one rank (hexbp_dist_*, NCCL
+// owned by the library; one process per GPU). Rank 0 makes the id with
+// nccl_unique_id() and the caller broadcasts its 128 bytes to the other ranks.
+using NcclId = std::array<unsigned char, 128>;
+inline NcclId nccl_unique_id() {
+  NcclId id{};
+  check(hexbp_dist_unique_id(id.data(), static_cast<int64_t>(id.size())));
+  return id;
+}
+
+class DistributedOperator {
+ public:
+  // This rank's share (balanced split of the element layers, rank order = z
+  // order) of the operator on build_box_mesh(global dims); collective.
+  DistributedOperator(BPKind kind, const HexMesh& global_mesh, int world, int rank, const NcclId& id,
+                      int device = 0, bool overlap = true) {
+    check(hexbp_dist_create_box(bp_code(kind), global_mesh.degree, global_mesh.dims.data(), global_mesh.extent.data(),
+                                global_mesh.deform_amplitude, world, rank, device, id.data(),
+                                static_cast<int64_t>(id.size()), overlap ? 0 : HEXBP_DIST_NO_OVERLAP, &h_));
+    check(hexbp_dist_info(h_, nullptr, &world_, &rank_, &n_, &owned_, &offset_));
+  }
+  ~DistributedOperator() {
+    if (h_) hexbp_dist_destroy(h_);
+  }
+  DistributedOperator(const DistributedOperator&) = delete;
+  DistributedOperator& operator=(const DistributedOperator&) = delete;
+
+  int size() const { return static_cast<int>(n_); }        // local L-vector length
+  int64_t owned_offset() const { return owned_; }          // plane 0 belongs to the rank below
+  int64_t global_offset() const { return offset_; }        // global index of local node 0
+  int world() const { return world_; }
+  int rank() const { return rank_; }
+  void set_mode(Mode m) { check(hexbp_dist_set_mode(h_, static_cast<int>(m))); }
+
+  // OperatorHandle::apply / ConstrainedOperator::apply on this rank's slice
+  // (w = the assembled local part of A u); collective
+  void apply(std::span<const double> u, std::vector<double>& w, bool constrained = false) const {
+    if (static_cast<int64_t>(u.size()) != n_) throw std::invalid_argument("apply: L-vector length mismatch");
+    w.resize(u.size());
+    check(hexbp_dist_apply_host(h_, u.data(), w.data(), n_, constrained ? 1 : 0));
+  }
+  void apply_device(const double* u, double* w, bool constrained = false, void* stream = nullptr) const {
+    check(hexbp_dist_apply(h_, u, w, constrained ? 1 : 0, stream));
+  }
+  // cg (solver.hpp:91-153) on the partition; every rank returns the same report
+  CGReport cg(std::span<const double> b, std::vector<double>& x, double rel_tol = 1e-8, int max_iter = 2000,
+              bool constrained = true) const {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (static_cast<int64_t>(b.size()) != n_ || x.size() != b.size())
+      throw std::invalid_argument("cg: x0 length mismatch");
+    if (max_iter < 0) throw std::invalid_argument("cg: max_iter must be >= 0");
+    std::vector<double> hist(static_cast<std::size_t>(max_iter) + 1);
+    hexbp_cg_report rep{};
+    check(hexbp_dist_cg_host(h_, b.data(), x.data(), n_, rel_tol, max_iter, constrained ? 1 : 0, &rep, hist.data()));
+    CGReport r;
+    r.iterations = rep.iterations;
+    r.converged = rep.converged != 0;
+    r.final_rel_residual = rep.final_rel_residual;
+    hist.resize(static_cast<std::size_t>(rep.iterations) + 1);
+    r.residual_history = std::move(hist);
+    r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return r;
+  }
+  hexbp_dist_t handle() const { return h_; }
+
+ private:
+  hexbp_dist_t h_ = nullptr;
+  int world_ = 1, rank_ = 0;
+  int64_t n_ = 0, owned_ = 0, offset_ = 0;
+};
+
 // run_bench's right-hand side (bench.hpp:234-243), BENCH_SEED default 20240101
 inline std::vector<double> bench_rhs(BPKind kind, int p, std::array<int, 3> dims, uint64_t seed = 20240101ull) {
   const int64_t n = static_cast<int64_t>(dims[0] * p + 1) * (dims[1] * p + 1) * (dims[2] * p + 1);

@@ -84,6 +84,20 @@ def lib() -> C.CDLL:
         "hexbp_interp_to_qpts": (C.c_int, [_vp, _vp, _vp, _vp]),
         "hexbp_interp_transpose": (C.c_int, [_vp, _vp, _vp, _vp]),
         "hexbp_cgd_update_r_fused": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+        "hexbp_workspace_reserve": (C.c_int, [_vp, C.c_int, C.c_int]),
+        "hexbp_dist_unique_id": (C.c_int, [_vp, C.c_int64]),
+        "hexbp_dist_create": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.POINTER(_vp)]),
+        "hexbp_dist_create_box": (C.c_int, [C.c_int, C.c_int, i3, _dp, C.c_double, C.c_int, C.c_int, C.c_int, _vp,
+                                            C.c_int64, C.c_int, C.POINTER(_vp)]),
+        "hexbp_dist_destroy": (None, [_vp]),
+        "hexbp_dist_info": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "hexbp_dist_set_mode": (C.c_int, [_vp, C.c_int]),
+        "hexbp_dist_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+        "hexbp_dist_cg": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, C.c_int, C.POINTER(CGReportC), _dp, _vp]),
+        "hexbp_dist_apply_host": (C.c_int, [_vp, _dp, _dp, C.c_int64, C.c_int]),
+        "hexbp_dist_cg_host": (C.c_int, [_vp, _dp, _dp, C.c_int64, C.c_double, C.c_int, C.c_int,
+                                         C.POINTER(CGReportC), _dp]),
     }
     dev_override = bool(os.environ.get("HEXBP_LIB"))  # A/B timing of older builds (tools/ab_time.py)
     for name, (res, args) in sig.items():

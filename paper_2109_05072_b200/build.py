@@ -15,7 +15,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhexbp_b200.so")
-SOURCES = ["apply.cu", "apply_exact.cu", "apply_mma.cu", "apply_mma5.cu", "cg.cu", "jacobi.cu", "multipass.cu", "fe_tools.cu", "setup.cu", "capi.cu", "basis.cpp"]
+SOURCES = ["apply.cu", "apply_exact.cu", "apply_mma.cu", "apply_mma5.cu", "overlap.cu", "cg.cu", "jacobi.cu",
+           "multipass.cu", "fe_tools.cu", "setup.cu", "capi.cu", "dist.cu", "basis.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -61,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xlinker", "--no-undefined", *objs,
-            "-o", LIB + ".tmp"]
+            "-lnccl", "-o", LIB + ".tmp"]
     subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -1242,8 +1242,8 @@ void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ki.fn, ki.nt, ki.smem);
 }
 
-cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
-                         double* dot_out, DevScalars* sc, cudaStream_t st, bool finish_ring) {
+ApplyArgs make_apply_args(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                          double* dot_out, DevScalars* sc) {
   ApplyArgs a{};
   a.u = u;
   a.w = w;
@@ -1269,6 +1269,14 @@ cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, d
   a.sc = sc;
   a.dot_out = dot_out;
   a.zlo_shared = s.z0 > 0;
+  a.zr0 = 0;
+  a.zr1 = s.dims[2];
+  return a;
+}
+
+cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                         double* dot_out, DevScalars* sc, cudaStream_t st, bool finish_ring) {
+  const ApplyArgs a = make_apply_args(s, ws, u, w, constrained, dot_out, sc);
   if (ws.multipass) {  // Backend::Multipass analog (reference arithmetic; CG reduces in cg.cu)
     if (dot_out || sc) return cudaErrorInvalidValue;
     return launch_apply_multipass(s, ws.mp_buf, u, w, constrained, st);

@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(NT, 2)
   const bool do_dot = A.col_dot != nullptr;
   const int col = blockIdx.x;
   const int ex = col % A.nx, ey = col / A.nx;
-  const int nz = A.nz;
+  const int nz = A.nz;              // elements per column of the slab (G column stride)
+  const int e0 = A.zr0, e1 = A.zr1;  // elements this launch marches (dist.cu overlap: sub-ranges)
   const LatLayout Lat(P, A.nx, A.ny);
 
   // Basis: B and D stay in shared memory for the whole kernel. The 8 x 8
@@ -186,13 +187,13 @@ __global__ void __launch_bounds__(NT, 2)
   __syncthreads();
   if (tid == 0) {
     mbar_arrive_expect_tx(bar, gbytes);
-    bulk_g2s(smem_u32(Gs), Gcol, gbytes, bar, pol);
-    if (nz > 1) prefetch_l2_bulk(Gcol + GSE, gbytes);
+    bulk_g2s(smem_u32(Gs), Gcol + e0 * GSE, gbytes, bar, pol);
+    if (e1 - e0 > 1) prefetch_l2_bulk(Gcol + (e0 + 1) * GSE, gbytes);
   }
   // u staging of element e into buffer e % NUB: thread (i,j) of the footprint
   // (tid < 64) copies its z-pencil into [k][j*8+i]
   auto fetch_u = [&](int e) {
-    if (e < nz && tid < N * N) {
+    if (e < e1 && tid < N * N) {
       const int i = tid & 7, j = tid >> 3;
       const uint32_t dst = smem_u32(Us + (e % NUB) * US_SZ + tid);
       const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
@@ -391,9 +392,16 @@ __global__ void __launch_bounds__(NT, 2)
       o[0] += top0;
       o[1] += top1;
     }
-    if (g == P && e + 1 < nz) {
+    if (g == P && e + 1 < e1) {
       carry[0] = o[0];
       carry[1] = o[1];
+      return;
+    }
+    // range ends inside the slab (dist.cu overlap): leave this launch's share
+    // of the plane for launch_carry_combine (no store, no dot)
+    double* cplane = g == P ? A.carry_hi : (g == 0 && e == e0 ? A.carry_lo : nullptr);
+    if (cplane != nullptr) {
+      *reinterpret_cast<double2*>(cplane + col * (N * N) + G * N + 2 * t) = make_double2(o[0], o[1]);
       return;
     }
     const int Z = e * P + g, Y = ey * P + G;
@@ -449,22 +457,22 @@ __global__ void __launch_bounds__(NT, 2)
   // Work map: Z'(j) on warp j (its carry registers), Z(0..4) on warp 11 and
   // Z(5..7) on warps 8..10, X(G) on warp G < 11, Y'(c) on warp c, Y(c) on
   // warp (c+9) % 12.
-  fetch_u(0);
-  fetch_u(1);
+  fetch_u(e0);
+  fetch_u(e0 + 1);
   cp_async_wait<0>();
   __syncthreads();
-  if (warp < N) phaseZ(0, warp);
+  if (warp < N) phaseZ(e0, warp);
   __syncthreads();
   if (warp < Q) phaseY(warp);
   __syncthreads();
-  for (int e = 0; e <= nz; ++e) {
+  for (int e = e0; e <= e1; ++e) {
     // ---- interval A_e
     fetch_u(e + 2);
-    if (tid == 0 && e + 2 < nz) prefetch_l2_bulk(Gcol + (e + 2) * GSE, gbytes);
+    if (tid == 0 && e + 2 < e1) prefetch_l2_bulk(Gcol + (e + 2) * GSE, gbytes);
     // Z'(e-1) and Z(e+1) first: they do not read G, so the G(e) transfer
     // issued in B_{e-1} has the longest time to land before X(e) waits on it
-    if (e >= 1 && warp < N) phaseZp(e - 1, warp);
-    if (e + 1 < nz) {
+    if (e > e0 && warp < N) phaseZp(e - 1, warp);
+    if (e + 1 < e1) {
       // warp 11: Z(0..4); warps 8..10: Z(5..7) beside their X group
       if (warp == NXW) {
         for (int j = 0; j < 5; ++j) phaseZ(e + 1, j);
@@ -472,20 +480,20 @@ __global__ void __launch_bounds__(NT, 2)
         phaseZ(e + 1, warp - 3);
       }
     }
-    if (e < nz && warp < NXW) {
-      mbar_wait_parity(bar, e & 1);
+    if (e < e1 && warp < NXW) {
+      mbar_wait_parity(bar, (e - e0) & 1);
       phaseX(warp);
     }
-    if (e == nz) break;
+    if (e == e1) break;
     __syncthreads();
     // ---- interval B_e
-    if (tid == 0 && e + 1 < nz) {  // X(e) consumed the G buffer: stream G(e+1)
+    if (tid == 0 && e + 1 < e1) {  // X(e) consumed the G buffer: stream G(e+1)
       fence_proxy_async();
       mbar_arrive_expect_tx(bar, gbytes);
       bulk_g2s(smem_u32(Gs), Gcol + (e + 1) * GSE, gbytes, bar, pol);
     }
     if (warp < Q) phaseYp(warp);
-    if (e + 1 < nz) {
+    if (e + 1 < e1) {
       // Y(c) on warp (c + 9) % NW
       const int c = warp >= 9 ? warp - 9 : warp + NW - 9;
       if (c < Q) phaseY(c);

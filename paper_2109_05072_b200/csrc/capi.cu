@@ -11,15 +11,9 @@
 #include <string>
 #include <vector>
 
+#include "capi_util.h"
 #include "internal.h"
 #include "ring.cuh"
-
-struct hexbp_setup_s {
-  hxb::Setup s;
-};
-struct hexbp_workspace_s {
-  hxb::Workspace w;
-};
 
 namespace hxb {
 
@@ -32,37 +26,6 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 using namespace hxb;
 
 namespace {
-
-int cuda_status(cudaError_t e, const char* where) {
-  if (e == cudaSuccess) return HEXBP_OK;
-  set_error(std::string(where) + ": " + cudaGetErrorString(e));
-  cudaGetLastError();  // clear sticky non-fatal errors
-  return e == cudaErrorMemoryAllocation ? HEXBP_OUT_OF_MEMORY : HEXBP_CUDA_ERROR;
-}
-
-#define CK(call)                                          \
-  do {                                                    \
-    cudaError_t _e = (call);                              \
-    if (_e != cudaSuccess) return cuda_status(_e, #call); \
-  } while (0)
-
-int invalid(const std::string& m) {
-  set_error(m);
-  return HEXBP_INVALID_ARGUMENT;
-}
-
-struct DeviceGuard {
-  int prev = 0;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    if (cur != prev) cudaSetDevice(prev);
-  }
-};
 
 int kind_of(int bp) { return bp == 1 ? KIND_MASS : (bp == 3 ? KIND_DIFF : KIND_COLLOC); }
 
@@ -202,6 +165,22 @@ int create_box(int bp, int p, const int gdims[3], int z0, int z1, const double e
     return HEXBP_DEGENERATE;
   }
   *out = h;
+  return HEXBP_OK;
+}
+
+int ensure_history(Workspace& w, int max_iter) {
+  if (max_iter + 1 <= w.history_cap) return HEXBP_OK;
+  CK(cudaFree(w.history));
+  w.history = nullptr;
+  w.history_cap = 0;
+  CK(cudaMalloc(&w.history, sizeof(double) * (max_iter + 1)));
+  w.history_cap = max_iter + 1;
+  return HEXBP_OK;
+}
+
+int ensure_diag_staging(Workspace& w) {
+  if (w.tmp_d) return HEXBP_OK;
+  CK(cudaMalloc(&w.tmp_d, sizeof(double) * w.s->nL));
   return HEXBP_OK;
 }
 
@@ -449,11 +428,21 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
   return HEXBP_OK;
 }
 
+int hexbp_workspace_reserve(hexbp_workspace_t wh, int max_iter, int host_staging) {
+  if (!wh || max_iter < 0) return invalid("workspace_reserve: bad argument");
+  Workspace& w = wh->w;
+  DeviceGuard g(w.device);
+  int rc = ensure_history(w, max_iter);
+  if (!rc && (host_staging & 1)) rc = ensure_host_staging(w);
+  if (!rc && (host_staging & 2)) rc = ensure_diag_staging(w);
+  return rc;
+}
+
 void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   if (!wh) return;
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
-  void* bufs[] = {w.mp_buf, w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.vec_partials,
+  void* bufs[] = {w.mp_buf, w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.tmp_d, w.vec_partials,
                   w.vec_done, w.history, w.dot_result};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -536,12 +525,12 @@ int hexbp_pcg_host(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, doubl
   if (rc) return rc;
   double* dd = nullptr;
   if (diag) {
-    CK(cudaMalloc(&dd, sizeof(double) * n));
+    if ((rc = ensure_diag_staging(w))) return rc;
+    dd = w.tmp_d;
     CK(cudaMemcpy(dd, diag, sizeof(double) * n, cudaMemcpyHostToDevice));
   }
   CK(stage_solve_inputs(w, b, x, n, nullptr));
   rc = pcg_run(h, wh, w.tmp_u, w.tmp_w, dd, rel_tol, max_iter, constrained, report, history, nullptr, w.ev_b);
-  if (dd) cudaFree(dd);
   if (rc == HEXBP_OK || rc == HEXBP_DIVERGENCE) CK(cudaMemcpy(x, w.tmp_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return rc;
 }
@@ -565,12 +554,8 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
   const Setup& s = h->s;
   Workspace& w = wh->w;
   DeviceGuard g(s.device);
-  if (max_iter + 1 > w.history_cap) {
-    CK(cudaFree(w.history));
-    w.history = nullptr;
-    w.history_cap = max_iter + 1;
-    CK(cudaMalloc(&w.history, sizeof(double) * w.history_cap));
-  }
+  int hrc = ensure_history(w, max_iter);  // no-op within the reserved capacity
+  if (hrc) return hrc;
   const int64_t n = s.nL;
   // Jacobi preconditioner for this solve (DevScalars::precond selects the
   // r.z recurrence of beta in the kernels' scalar logic)
@@ -689,11 +674,9 @@ int hexbp_cgd_finish(hexbp_workspace_t wh, int op, const double* gathered, int w
   if (!wh || !gathered || world < 1 || op < 0 || op > 2) return invalid("cgd_finish: bad argument");
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
-  if (op == 0 && max_iter + 1 > w.history_cap) {
-    CK(cudaFree(w.history));
-    w.history = nullptr;
-    w.history_cap = max_iter + 1;
-    CK(cudaMalloc(&w.history, sizeof(double) * w.history_cap));
+  if (op == 0) {
+    const int rc = ensure_history(w, max_iter);
+    if (rc) return rc;
   }
   CK(launch_cgd_finish(w, op, gathered, world, rel_tol, max_iter, static_cast<cudaStream_t>(stream)));
   return HEXBP_OK;

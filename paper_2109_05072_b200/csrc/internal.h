@@ -74,6 +74,15 @@ struct ApplyArgs {
   double* lat_x;            // fast mode: latX (ring.cuh)
   int zlo_shared;           // z-slab partition: node plane Z = 0 is owned by the rank below (its
                             // constrained nodes' u.u share of p.Ap is counted there)
+  // Element range [zr0, zr1) of every column this launch marches (default
+  // [0, nz)); kernels without range support (apply_overlap_supported) ignore it.
+  int zr0, zr1;
+  // Non-null: the range's bottom (carry_lo) / top (carry_hi) node plane is
+  // not stored but left as this launch's share in [column][(p+1)^2] (j-major
+  // footprint order), to be summed with the neighbouring launch's share by
+  // launch_carry_combine -- the multi-GPU overlap of dist.cu.
+  double* carry_lo;
+  double* carry_hi;
 };
 
 struct Setup {
@@ -113,6 +122,7 @@ struct Workspace {
   double* Ap = nullptr;
   double* tmp_u = nullptr;  // host-API staging
   double* tmp_w = nullptr;
+  double* tmp_d = nullptr;  // host-API Jacobi diagonal staging
   double* vec_partials = nullptr;
   unsigned int* vec_done = nullptr;
   double* history = nullptr;
@@ -134,9 +144,30 @@ struct Workspace {
 // ---- apply.cu
 // finish_ring = false leaves the ring nodes of w as lateral partials (CG fast
 // mode: launch_cg_update_r sums them).
+ApplyArgs make_apply_args(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                          double* dot_out, DevScalars* sc);
 cudaError_t launch_apply(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
                          double* dot_out, DevScalars* sc, cudaStream_t st, bool finish_ring = true);
 int fixup_grid(const Setup& s);
+// ---- overlap.cu: boundary / interior split of a slab apply (dist.cu overlap)
+struct OverlapBuffers {
+  double* carry;         // overlap_carry_doubles(s)
+  double* slots;         // [3] p.Ap partials of the boundary (2) and interior launches
+  double* coldot;        // [3 * ncols] per-launch column partials
+  unsigned int* tickets; // [4] zeroed last-CTA tickets
+  double* partials;      // [overlap_partials_capacity()]
+};
+bool apply_overlap_supported(const Setup& s);
+int64_t overlap_carry_doubles(const Setup& s);
+int overlap_partials_capacity();
+cudaError_t launch_apply_boundary(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                                  const OverlapBuffers& ob, cudaStream_t st);
+cudaError_t launch_apply_interior(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                                  const OverlapBuffers& ob, cudaStream_t st);
+// inner planes from the carries + their p.Ap share; *out = the rank's whole p.Ap share
+cudaError_t launch_carry_combine(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
+                                 const OverlapBuffers& ob, double* out, cudaStream_t st);
+
 // ---- apply_mma.cu (FP64 tensor-core kernel, BP3 p = 7)
 bool mma_kernel_applies(const Setup& s);
 // ---- apply_mma5.cu (FP64 tensor-core kernel, BP5 p = 7)

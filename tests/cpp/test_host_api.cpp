@@ -79,7 +79,12 @@ int main() {
   op.workspace().set_mode(Mode::Fast);
   std::vector<double> x2(b.size(), 0.0);
   const CGReport rf = cg(cop, b, x2, 1e-8, 2000);
-  EXPECT(std::abs(rf.iterations - 235) <= 1, "fast mode iterations %d", rf.iterations);
+  // fast mode: the reference's 235 iterations; the final residual moves by
+  // 1.13e-10 (this case is one of the two documented fast-mode exceptions,
+  // tests/test_gpu_parity.py FAST_EXCEPTIONS, profiles/r2_parity_perturb.json)
+  EXPECT(rf.iterations == 235 && rf.converged, "fast mode iterations %d", rf.iterations);
+  EXPECT(std::fabs(rf.final_rel_residual - 9.757368339832182e-09) <= 1.5e-10, "fast mode final %.17g",
+         rf.final_rel_residual);
   // Backend::Multipass analog (the reference's multipass operation order, so
   // tolerance-level against the fused apply) and the workspace queries of
   // operator.hpp:193-201

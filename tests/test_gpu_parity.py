@@ -164,23 +164,36 @@ def test_cg_matches_reference(golden_cg, name):
     assert np.sqrt(oracle.dot(x, x)) == c["x_norm"]
 
 
+# Fast-mode (throughput path) CG against the reference's own solves. north_star:
+# the same iteration count and |d final rel residual| <= 1e-10 -- met by every
+# golden but two (profiles/r2_parity_fast.json). For those two, a perturbation
+# of the reference operator by 1e-16 relative per entry -- below one ulp, the
+# size of the fast kernels' FMA/DMMA rounding -- already moves the final
+# residual by 1.2e-10 (bp3_p3_12) and 1.6-2.3e-10 (bp5_p7_6), and by 5e-16 it
+# changes bp5_p7_6's count to 420 (tools/parity_perturb.py ->
+# profiles/r2_parity_perturb.json); the reference-order reductions of
+# HEXBP_MODE_FAST_OPERATOR do not help (10 of 14 cases meet the bar there).
+# Their fast-mode deviations are deterministic and pinned here; only the
+# bit-exact reference mode (test_cg_matches_reference) can match them.
+FAST_EXCEPTIONS = {"bp3_p3_12_a0.1": (0, 1.5e-10), "bp5_p7_6_a0.1": (1, 2.5e-10)}
+
+
 @pytest.mark.parametrize("name", ["bp3_p3_12_a0.1", "bp3_p7_6_a0.1", "bp5_p7_6_a0.1", "bp1_p7_6_a0.1",
-                                  "bp3_p5_5x4x7_a0.1", "cfg1_a0", "cfg1_a0.1"])
+                                  "bp3_p5_5x4x7_a0.1", "cfg1_a0", "cfg1_a0.1", "cfg1_fixed50", "bp1_p2_fixed20"])
 def test_cg_fast_mode_tracks_reference(golden_cg, name):
-    """Fast mode (FMA kernels, fused p.Ap): the operator differs from the
-    reference by ~1e-16 per entry; CG at p=7 amplifies such perturbations
-    (tools/parity_diag.py: 1e-15 relative noise moves the final residual by
-    ~5e-11), so the count is checked to +-1 iteration and the final residual
-    to 5e-10 here, while reference mode (above) is bit-exact."""
+    """Fast mode (DMMA / FMA kernels, fused p.Ap, tree reductions): equal
+    iteration counts and |d final| <= 1e-10 (north_star), exceptions above."""
     c = golden_cg[name]
     op = op_for(c["bp"], c["p"], c["dims"], c["a"], mode="fast")
     b = hx.bench_rhs(c["bp"], c["p"], c["dims"])
     x = np.zeros(op.size())
     A = hx.ConstrainedOperator(op) if c["bp"] != 1 else op
     rep = hx.cg(A, b, x, rel_tol=c["rel_tol"], max_iter=c["max_iter"], mode="fast")
-    assert abs(rep.iterations - c["iterations"]) <= 1
-    assert rep.converged
-    assert abs(rep.final_rel_residual - c["final_rel_residual"]) <= 5e-10
+    d_iter, d_final = FAST_EXCEPTIONS.get(name, (0, 1e-10))
+    assert abs(rep.iterations - c["iterations"]) <= d_iter, (rep.iterations, c["iterations"])
+    assert rep.converged == c["converged"]
+    assert abs(rep.final_rel_residual - c["final_rel_residual"]) <= d_final, (rep.final_rel_residual,
+                                                                               c["final_rel_residual"])
     assert abs(rep.residual_history[0] - c["residual_history"][0]) <= 1e-13 * c["residual_history"][0]
 
 

@@ -108,14 +108,19 @@ def test_device_pcg_fast_mode(bp, p, dims, a):
     rep = hx.cg(A, b, x, rel_tol=1e-8, max_iter=2000, diag=d, mode="fast")
     ref = o.cg(o.bench_rhs(), rel_tol=1e-8, max_iter=2000, constrained=con, diag=o.jacobi_diagonal(con))
     assert rep.converged
-    assert abs(rep.iterations - ref["iterations"]) <= 1
-    assert abs(rep.final_rel_residual - ref["final_rel_residual"]) <= 5e-10
+    # north_star bar: same count, |d final| <= 1e-10 (profiles/r2_parity_fast.json)
+    assert rep.iterations == ref["iterations"]
+    assert abs(rep.final_rel_residual - ref["final_rel_residual"]) <= 1e-10
     assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
     # plain CG afterwards on the same workspace is unaffected (preconditioner state cleared)
     x2 = torch.zeros_like(b)
     rep2 = hx.cg(A, b, x2, rel_tol=1e-8, max_iter=2000, mode="fast")
-    ref2 = o.cg(o.bench_rhs(), rel_tol=1e-8, max_iter=2000, constrained=con)
-    assert abs(rep2.iterations - ref2["iterations"]) <= 1
+    # ... bit for bit the solve of a fresh workspace
+    _, fresh = _op(bp, p, dims, a, "fast")
+    x3 = torch.zeros_like(b)
+    rep3 = hx.cg(hx.ConstrainedOperator(fresh) if con else fresh, b, x3, rel_tol=1e-8, max_iter=2000, mode="fast")
+    assert rep2.iterations == rep3.iterations
+    assert np.array_equal(rep2.residual_history, rep3.residual_history) and torch.equal(x2, x3)
 
 
 @pytest.mark.gpu

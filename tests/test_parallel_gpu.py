@@ -85,5 +85,10 @@ def test_ranks_on_one_gpu_match_single_domain(world, case, mode):
     for r in res.values():
         assert r["apply0"] < 1e-13 and r["apply1"] < 1e-13
         assert r["iters"] == res[0]["iters"] and r["final"] == res[0]["final"]
-        assert abs(r["iters"] - r["ref_iters"]) <= 1
+        # the slab CG reduces in rank order, the single-domain fast CG in its own
+        # tree: same count; the residuals of these two fast-mode solves agree up to
+        # the chaotic amplification of rounding (bp5 p=4: 3.4e-10, bp1 p=2: 6.2e-10). The north-star
+        # comparison against the reference itself: test_dist_nccl.py, test_gpu_parity.py
+        assert r["iters"] == r["ref_iters"]
+        assert abs(r["final"] - r["ref_final"]) <= (1e-10 if mode == "reference" else 1e-9)
         assert r["xerr"] < 1e-7

@@ -62,6 +62,16 @@ def default_dims(p: int):
     return (e, e, e)
 
 
+def kernel_sources_sha(files) -> str:
+    """Hash stamp of the kernel sources a profile was captured on (profiles/traffic.json)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in files:
+        h.update(open(os.path.join(ROOT, "paper_2109_05072_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -146,50 +156,43 @@ class ClockSampler:
                 "reasons": sorted({x for r in self.rows for x in r[2]}), "samples": len(self.rows)}
 
 
-def cpu_baseline(bp: int, p: int, steps: int = 3):
-    """The reference's own run_bench (oracle/_ref) on this host, all cores,
-    bounded sample: same bp/p on ~2M DOFs, fixed CG iterations."""
+def cpu_baseline(bp: int, p: int, iters: int = 20, warmup: int = 1, repeats: int = 3, cfg1: bool = True) -> dict:
+    """The reference's own run_bench (oracle/_ref, unmodified headers compiled in
+    place) on this host as BASELINE.md section 2 plans it: same bp/p at ~10M DOFs,
+    `iters` fixed CG iterations, OMP_NUM_THREADS = physical cores with
+    OMP_PROC_BIND=close / OMP_PLACES=cores, plus BASELINE configs[0] in full
+    (cfg1). Run in a subprocess so the OpenMP settings take effect."""
     import oracle
+    from oracle import cpu_baseline as cb
 
     oracle.build()
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    e = 1
-    while ((e + 1) * p + 1) ** 3 <= 2_000_000:
-        e += 1
-    cfg = {"bp": f"bp{bp}", "degrees": [p], "dims": [e, e, e], "backends": ["fused"], "fixed_cg_iters": steps,
-           "warmup_repeats": 1, "timed_repeats": 2, "threads": cores}
-    kind = "reference"
-    try:
-        rec = oracle.ref_run_bench(json.dumps(cfg))[0]
-        gdofs = rec["throughput"] / 1e9
-        threads = rec["threads"]
-    except (FileNotFoundError, OSError):
-        kind = "port"
-        o = oracle.Oracle(bp, p, (e, e, e), 0.0)
-        b = o.bench_rhs()
-        o.cg(b, rel_tol=0.0, max_iter=1, constrained=bp != 1)
-        t = time.perf_counter()
-        o.cg(b, rel_tol=0.0, max_iter=steps, constrained=bp != 1)
-        gdofs = o.n * steps / (time.perf_counter() - t) / 1e9
-        threads = cores
-    return {"value": gdofs, "unit": "GDOF/s", "cores": threads, "kind": kind,
-            "sample": f"bp{bp} p={p} {e}^3 elements ({(e * p + 1) ** 3} DOFs), {steps} fixed CG iterations, "
-                      f"best of 2 after 1 warm-up, reference run_bench (bench.hpp:214-295), OMP threads={threads}"}
+    cores = cb.physical_cores()
+    env = dict(os.environ, OMP_NUM_THREADS=str(cores), OMP_PROC_BIND="close", OMP_PLACES="cores")
+    cmd = [sys.executable, "-m", "oracle.cpu_baseline", "--bp", str(bp), "--p", str(p), "--iters", str(iters),
+           "--warmup", str(warmup), "--repeats", str(repeats)] + (["--cfg1"] if cfg1 else [])
+    out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=1200)
+    if out.returncode != 0:
+        raise RuntimeError((out.stderr or out.stdout)[-300:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cb = cpu_baseline(args.bp, args.p, steps=max(1, min(args.steps, 5)))
+    # the reference's own CPU path on this host's cores: K fixed CG iterations
+    # per solve (the steps), W warm-up solves, best of 3 timed solves, on the
+    # ~10M-DOF sample of the same bp / p (BASELINE.md section 2)
+    cb = cpu_baseline(args.bp, args.p, iters=args.steps, warmup=max(1, min(args.warmup, 3)), repeats=3, cfg1=False)
     dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else default_dims(args.p)
+    hs = cb["headline_sample"]
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GDOF/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "steps": hs["fixed_cg_iters"], "warmup": hs["warmup_solves"] * hs["fixed_cg_iters"],
+        "ms_per_step": hs["best_solve_s"] / hs["fixed_cg_iters"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"bp{args.bp} p={args.p} box {dims[0]}x{dims[1]}x{dims[2]} per GPU (CPU arm: bounded "
-                               f"sample, see cpu_baseline.sample)", "bp": args.bp, "p": args.p},
+        "config": {"workload": f"bp{args.bp} p={args.p}: the ours arm runs {dims[0]}x{dims[1]}x{dims[2]} per GPU; "
+                               f"this CPU arm a bounded sample of it ({cb['sample']})", "bp": args.bp, "p": args.p},
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -303,12 +306,17 @@ def main():
     b_op, b_it, nL, E = algorithmic_bytes(bp, p, dims)
     peak, peak_kind = load_peaks()
     achieved = b_op / t_apply / 1e9
-    traffic = None
+    # DRAM bytes per launch from the committed ncu capture -- used only if it was
+    # taken on the kernel sources now built (hash stamp), else reported stale
+    traffic, traffic_note = None, "no capture for this configuration"
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         tr = json.load(open(prof)).get(f"bp{bp}_p{p}_{dims[0]}x{dims[1]}x{dims[2]}")
         if tr:
-            traffic = tr.get("dram_bytes_per_launch")
+            if tr.get("source_sha256_16") == kernel_sources_sha(tr.get("kernel_sources", [])):
+                traffic, traffic_note = tr.get("dram_bytes_per_launch"), tr.get("source")
+            else:
+                traffic_note = "stale: the capture's kernel sources differ from the built ones"
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     bh = torch.from_numpy(b_host).pin_memory()
@@ -340,7 +348,7 @@ def main():
                    "deform_amplitude": args.amplitude, "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (factors %.2f GB)" % (setup.factor_bytes / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": traffic_note,
                      "kernel": ("bp3_p7_mma_kernel (DMMA)" if (bp == 3 and p == 7) else "bp_apply_kernel") +
                                " (ring nodes as column partials, summed by the CG r-update)",
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",

@@ -30,7 +30,8 @@ _dp = C.POINTER(C.c_double)
 def build(force: bool = False) -> None:
     """Compile the C restatement (and oracle/_ref when the reference exists)."""
     if force or not os.path.exists(ORACLE_SO) or (
-        os.path.isdir("/root/reference") and not os.path.exists(REF_SO)
+        os.path.isdir("/root/reference") and not all(os.path.exists(REF_SO.replace(".so", v + ".so"))
+                                                     for v in ("", "_x86-64-v3", "_x86-64-v4"))
     ):
         subprocess.run(["make", "-C", HERE, "all"], check=True, stdout=subprocess.DEVNULL)
 
@@ -257,9 +258,9 @@ def dot(a, b) -> float:
     return float(oracle_lib().or_dot(_ptr(a), _ptr(b), a.size))
 
 
-def ref_run_bench(config_json: str, cap: int = 64):
+def ref_run_bench(config_json: str, cap: int = 64, so: str = REF_SO):
     """Reference run_bench through its JSON parser (bench.hpp:93-153,214-295)."""
-    lib = _Lib.load(REF_SO)
+    lib = _Lib.load(so)
     f = lib.ref_run_bench_json
     f.restype = C.c_int
     f.argtypes = [C.c_char_p, _dp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.c_int]

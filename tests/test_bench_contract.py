@@ -29,3 +29,6 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["bp"] == 3 and d["config"]["p"] == 7
+    # the arm reports the steps it ran: 3 fixed CG iterations per timed solve
+    assert d["steps"] == 3 and d["cpu_baseline"]["headline_sample"]["fixed_cg_iters"] == 3
+    assert d["cpu_baseline"]["omp"]["OMP_PROC_BIND"] == "close" and d["cpu_baseline"]["omp"]["OMP_PLACES"] == "cores"

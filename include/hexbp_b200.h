@@ -82,6 +82,14 @@ int hexbp_setup_create(int bp, int p, int q, const int dims[3], const double* B,
                        const double* factors_aos, int device, hexbp_setup_t* out);
 
 void hexbp_setup_destroy(hexbp_setup_t s);
+/* The device kernels compute the structured restriction arithmetically
+ * (global id of node (i,j,k) of element (ex,ey,ez), mesh.hpp:74-82) instead
+ * of streaming ElementRestriction::elem_to_global (restriction.hpp:22-53).
+ * A caller adopting a reference OperatorSetup passes its table here: OK iff it
+ * is exactly that numbering for this setup's box (slab: the global ids of its
+ * element layers); HEXBP_INVALID_ARGUMENT (with the first mismatching slot in
+ * hexbp_last_error) otherwise -- a non-box restriction would give wrong results. */
+int hexbp_setup_check_restriction(hexbp_setup_t s, const int32_t* elem_to_global, int64_t n);
 int hexbp_setup_get_info(hexbp_setup_t s, hexbp_setup_info* out);
 /* B, D as used by the kernels (q x (p+1) row-major). */
 int hexbp_setup_basis(hexbp_setup_t s, double* B, double* D);

@@ -23,6 +23,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhexbp_ref.so")
+# the drop-in test binary (tests/cpp/test_dropin_ref.cpp against the reference headers)
+DROPIN_BIN = os.path.join(HERE, "_ref", "test_dropin_ref")
+DROPIN_SRC = os.path.join(os.path.dirname(HERE), "tests", "cpp", "test_dropin_ref.cpp")
 
 _dp = C.POINTER(C.c_double)
 
@@ -30,8 +33,9 @@ _dp = C.POINTER(C.c_double)
 def build(force: bool = False) -> None:
     """Compile the C restatement (and oracle/_ref when the reference exists)."""
     if force or not os.path.exists(ORACLE_SO) or (
-        os.path.isdir("/root/reference") and not all(os.path.exists(REF_SO.replace(".so", v + ".so"))
-                                                     for v in ("", "_x86-64-v3", "_x86-64-v4"))
+        os.path.isdir("/root/reference") and not (
+            all(os.path.exists(REF_SO.replace(".so", v + ".so")) for v in ("", "_x86-64-v3", "_x86-64-v4"))
+            and os.path.exists(DROPIN_BIN) and os.path.getmtime(DROPIN_BIN) >= os.path.getmtime(DROPIN_SRC))
     ):
         subprocess.run(["make", "-C", HERE, "all"], check=True, stdout=subprocess.DEVNULL)
 

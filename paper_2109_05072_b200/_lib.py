@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
         "hexbp_interp_transpose": (C.c_int, [_vp, _vp, _vp, _vp]),
         "hexbp_cgd_update_r_fused": (C.c_int, [_vp, C.c_int, _vp, _vp]),
         "hexbp_workspace_reserve": (C.c_int, [_vp, C.c_int, C.c_int]),
+        "hexbp_setup_check_restriction": (C.c_int, [_vp, _vp, C.c_int64]),
         "hexbp_dist_unique_id": (C.c_int, [_vp, C.c_int64]),
         "hexbp_dist_create": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.POINTER(_vp)]),
         "hexbp_dist_create_box": (C.c_int, [C.c_int, C.c_int, i3, _dp, C.c_double, C.c_int, C.c_int, C.c_int, _vp,

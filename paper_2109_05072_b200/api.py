@@ -240,8 +240,11 @@ class OperatorSetup:
         return out
 
     @classmethod
-    def from_reference(cls, kind, p: int, dims, B, D, factors_aos, device: int = 0) -> "OperatorSetup":
-        """Adopt a host OperatorSetup's tables (drop-in path)."""
+    def from_reference(cls, kind, p: int, dims, B, D, factors_aos, device: int = 0,
+                       elem_to_global=None) -> "OperatorSetup":
+        """Adopt a host OperatorSetup's tables (drop-in path). ``elem_to_global``
+        (ElementRestriction, restriction.hpp:22-53), when given, is checked to be
+        the structured box numbering the kernels compute (ValueError otherwise)."""
         kind = BPKind(kind)
         q = default_quad_points(kind, p)
         B = np.ascontiguousarray(B, np.float64)
@@ -250,7 +253,16 @@ class OperatorSetup:
         h = C.c_void_p()
         _check(_lib.lib().hexbp_setup_create(int(kind), p, q, _i3(dims), B.ctypes.data_as(_dp),
                                              D.ctypes.data_as(_dp), F.ctypes.data_as(_dp), device, C.byref(h)))
-        return cls(h.value, device)
+        s = cls(h.value, device)
+        if elem_to_global is not None:
+            s.check_restriction(elem_to_global)
+        return s
+
+    def check_restriction(self, elem_to_global) -> None:
+        """hexbp_setup_check_restriction: ValueError unless the table is the
+        structured numbering of this box (mesh.hpp:74-82)."""
+        t = np.ascontiguousarray(elem_to_global, np.int32)
+        _check(_lib.lib().hexbp_setup_check_restriction(self._h, t.ctypes.data_as(C.c_void_p), t.size))
 
 
 def make_setup(kind, mesh: HexMesh, device: int = 0) -> OperatorSetup:
@@ -439,8 +451,10 @@ def make_operator(kind, backend: Backend, mesh: HexMesh, device: int = 0) -> Ope
 
 class ConstrainedOperator:
     """w = P A P u + (I - P) u (solver.hpp:48-74). The device kernel applies the
-    mask by a grid-boundary test, i.e. the homogeneous box-surface constraints
-    of boundary_bcs(mesh); other BC sets are rejected."""
+    mask by a grid-boundary test, i.e. the box-surface constraint set of
+    boundary_bcs(mesh); other dof sets are rejected. The constraint values are
+    accepted and ignored, as the reference's apply ignores them (w = u on the
+    essential dofs, solver.hpp:60-65)."""
 
     def __init__(self, op: OperatorHandle, bcs: Optional[BCSet] = None):
         self._op = op
@@ -450,8 +464,6 @@ class ConstrainedOperator:
             mesh = HexMesh(s.dims, s.p)
             if s.dims != s.gdims or not np.array_equal(np.asarray(bcs.dofs), boundary_nodes(mesh)):
                 raise ValueError("ConstrainedOperator: the CUDA backend supports the box-surface BCSet only")
-            if np.any(np.asarray(bcs.values) != 0.0):
-                raise ValueError("ConstrainedOperator: homogeneous constraints only")
         self._bcs = bcs
 
     def size(self) -> int:

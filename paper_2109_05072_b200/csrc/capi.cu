@@ -277,6 +277,32 @@ int hexbp_setup_create(int bp, int p, int q, const int dims[3], const double* B,
   return HEXBP_OK;
 }
 
+int hexbp_setup_check_restriction(hexbp_setup_t h, const int32_t* elem_to_global, int64_t n) {
+  if (!h || (!elem_to_global && n)) return invalid("check_restriction: null argument");
+  const Setup& s = h->s;
+  const int p = s.p, nn = p + 1;
+  const int64_t nen = static_cast<int64_t>(nn) * nn * nn;
+  if (n != s.E * nen)
+    return invalid("check_restriction: table length " + std::to_string(n) + " != elements x (p+1)^3 = " +
+                   std::to_string(s.E * nen));
+  const int64_t gx = static_cast<int64_t>(s.gdims[0]) * p + 1, gy = static_cast<int64_t>(s.gdims[1]) * p + 1;
+  int64_t pos = 0;
+  for (int ez = s.z0; ez < s.z0 + s.dims[2]; ++ez)  // mesh.hpp:74-82 element and node order
+    for (int ey = 0; ey < s.dims[1]; ++ey)
+      for (int ex = 0; ex < s.dims[0]; ++ex)
+        for (int k = 0; k <= p; ++k)
+          for (int j = 0; j <= p; ++j)
+            for (int i = 0; i <= p; ++i, ++pos) {
+              const int64_t g = (static_cast<int64_t>(ex) * p + i) + gx * ((static_cast<int64_t>(ey) * p + j) +
+                                                                           gy * (static_cast<int64_t>(ez) * p + k));
+              if (elem_to_global[pos] != g)
+                return invalid("check_restriction: elem_to_global[" + std::to_string(pos) + "] = " +
+                               std::to_string(elem_to_global[pos]) + ", the structured box numbering has " +
+                               std::to_string(g) + " (the device kernels support box meshes only)");
+            }
+  return HEXBP_OK;
+}
+
 void hexbp_setup_destroy(hexbp_setup_t h) {
   if (!h) return;
   DeviceGuard g(h->s.device);

@@ -71,3 +71,41 @@ def test_host_apply_into_foreign_outputs():
     wrong = np.zeros(n + 1)
     out = op.apply(u, wrong)  # wrong size: a fresh array is returned, as the reference resizes
     assert out.size == n and np.all(wrong == 0.0)
+
+
+def test_bc_values_are_accepted_and_ignored():
+    """solver.hpp:60-65: the constrained apply copies u on the essential dofs;
+    boundary_bcs(mesh, value) values are not used (the reference accepts any)."""
+    mesh = hx.build_box_mesh((2, 3, 2), 2, (1, 1, 1), 0.1)
+    op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind.BP3, mesh))
+    u = random_vector(4, op.size())
+    w0 = hx.ConstrainedOperator(op).apply(u)
+    for value in (0.0, 1.0, -3.5):
+        assert np.array_equal(hx.ConstrainedOperator(op, hx.boundary_bcs(mesh, value)).apply(u), w0)
+
+
+def _structured_table(dims, p):
+    """mesh.hpp:74-82 numbering, restated with numpy for the check."""
+    gx, gy = dims[0] * p + 1, dims[1] * p + 1
+    n = np.arange(p + 1)
+    out = []
+    for ez in range(dims[2]):
+        for ey in range(dims[1]):
+            for ex in range(dims[0]):
+                k, j, i = np.meshgrid(n, n, n, indexing="ij")
+                out.append(((ex * p + i) + gx * ((ey * p + j) + gy * (ez * p + k))).ravel())
+    return np.concatenate(out).astype(np.int32)
+
+
+def test_reference_setup_restriction_is_validated(golden_equiv):
+    idx, arr = golden_equiv
+    case = next(c for c in idx if "error" not in c and c["bp"] == 3)
+    k, dims, p = case["key"], case["dims"], case["p"]
+    table = _structured_table(dims, p)
+    s = hx.OperatorSetup.from_reference(3, p, dims, arr[k + "/B"], arr[k + "/D"], arr[k + "/G"], elem_to_global=table)
+    bad = table.copy()
+    bad[[1, 2]] = bad[[2, 1]]
+    with pytest.raises(ValueError):
+        s.check_restriction(bad)
+    with pytest.raises(ValueError):
+        s.check_restriction(table[:-1])

@@ -34,9 +34,9 @@ namespace {
 
 constexpr int VT = 256;
 constexpr int CHUNK = 4096;          // detail::kReductionBlock (dense.hpp:52)
-constexpr int CPB = 32;              // chunks per CTA (one per lane of warp 0)
-constexpr int TILE = 128;            // elements per chunk per tile
-constexpr int TSTRIDE = TILE + 1;    // smem row stride (conflict-free column walk)
+constexpr int RVT = 128;             // blocked_reduce_kernel: threads per CTA
+constexpr int RT = 32;               // entries per chunk per tile (one coalesced 256-byte row)
+constexpr int CPW = 16;              // chunks per warp (more warps, more loads in flight)
 
 #define DM(a, b) __dmul_rn((a), (b))
 #define DA(a, b) __dadd_rn((a), (b))
@@ -70,6 +70,36 @@ __device__ __forceinline__ double serial_sum(const double* part, long long n) {
   return s;
 }
 
+// The same sequential chunk-order sum by thread 0 of the (last) CTA, fed
+// from shared memory: the CTA stages the partials in double-buffered tiles
+// (coalesced loads by every thread) while thread 0 runs the dependent add
+// chain over the previous tile -- L2 latency off the chain. `buf`: >= 2 * RSB doubles.
+constexpr int RSB = 1024;
+__device__ double block_serial_sum(const double* part, long long n, double* buf) {
+  double s = 0.0;
+  const long long ntiles = (n + RSB - 1) / RSB;
+  auto stage = [&](long long t) {
+    double* dst = buf + (t & 1) * RSB;
+    for (int i = threadIdx.x; i < RSB; i += blockDim.x) {
+      const long long g = t * RSB + i;
+      dst[i] = g < n ? __ldcg(part + g) : 0.0;
+    }
+  };
+  if (ntiles > 0) stage(0);
+  __syncthreads();
+  for (long long t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) stage(t + 1);
+    if (threadIdx.x == 0) {
+      const double* src = buf + (t & 1) * RSB;
+      const int m = static_cast<int>(n - t * RSB < RSB ? n - t * RSB : RSB);
+#pragma unroll 16
+      for (int i = 0; i < m; ++i) s = DA(s, src[i]);
+    }
+    __syncthreads();
+  }
+  return s;
+}
+
 enum Op : int { OP_DOT = 0, OP_PAP = 1, OP_INIT = 2, OP_UPDATE_R = 3, OP_RZ = 4 };
 
 // Blocked exact reduction with an optional fused elementwise update.
@@ -81,68 +111,97 @@ enum Op : int { OP_DOT = 0, OP_PAP = 1, OP_INIT = 2, OP_UPDATE_R = 3, OP_RZ = 4 
 // With a Jacobi diagonal `dv`, OP_INIT stores p = z = r / diag.
 __device__ void scalar_logic(int op, double tot, DevScalars* sc, double* hist, double rel_tol, int max_iter);
 
+// Products / fused updates of one element (reference arithmetic, unfused).
+template <int OP>
+__device__ __forceinline__ double elem_op(double x, double y, long long g, double alpha, double* w0, double* w1,
+                                          const double* dv) {
+  if (OP == OP_DOT || OP == OP_PAP) return DM(x, y);
+  if (OP == OP_RZ) return DM(x, DD(x, y));  // r * (r / diag)
+  if (OP == OP_INIT) {
+    const double r = DS(x, y);  // r = b - Ap (solver.hpp:103)
+    w0[g] = r;
+    w1[g] = dv ? DD(r, dv[g]) : r;  // z = r / diag (or r); p = z (solver.hpp:105-109,123)
+    return DM(r, r);
+  }
+  const double r = DS(x, DM(alpha, y));  // r -= alpha * Ap (solver.hpp:133)
+  w0[g] = r;
+  return DM(r, r);
+}
+
+// Blocked exact reduction (deterministic_dot's order: every 4096-entry chunk
+// summed sequentially from 0.0, chunk partials summed in chunk order by the
+// last CTA, dense.hpp:52-81) with an optional fused elementwise update.
+// A warp owns 32 consecutive chunks; lane c sums chunk c. Per tile of RT
+// entries the warp loads each of its chunks' RT-entry segments coalesced (one
+// 256-byte row per load), computes the products / fused updates there (the
+// updated vectors are written coalesced) and transposes the products through
+// a per-warp shared tile; lane c then adds its row in order while the next
+// tile's loads are in flight. No CTA barrier: warps run independently.
 // `owned` >= 0: elementwise updates run over [0, n) but only entries
 // [owned, n) enter the sum (multi-GPU slabs: the bottom interface plane is
 // owned by the rank below); the rank partial is written to *out (dist mode).
 template <int OP>
-__global__ void __launch_bounds__(VT) blocked_reduce_kernel(const double* a, const double* b, double* w0,
-                                                            double* w1, long long n, double* part,
-                                                            unsigned int* done, DevScalars* sc, double* hist,
-                                                            double* out, double rel_tol, int max_iter,
-                                                            long long owned = -1, const double* dv = nullptr) {
-  __shared__ double prod[CPB * TSTRIDE];
+__global__ void __launch_bounds__(RVT) blocked_reduce_kernel(const double* a, const double* b, double* w0,
+                                                             double* w1, long long n, double* part,
+                                                             unsigned int* done, DevScalars* sc, double* hist,
+                                                             double* out, double rel_tol, int max_iter,
+                                                             long long owned = -1, const double* dv = nullptr) {
+  __shared__ double tile[RVT / 32][CPW * (RT + 1)];  // also the staging buffer of the final sum
+  static_assert(RVT / 32 * CPW * (RT + 1) >= 2 * RSB, "block_serial_sum buffer");
   const bool dist = owned >= 0;
   const long long lo = dist ? owned : 0;
   if (OP == OP_PAP || OP == OP_UPDATE_R || OP == OP_RZ) {
     if (*(volatile int*)&sc->status != ST_RUNNING) return;
   }
   const double alpha = OP == OP_UPDATE_R ? sc->alpha : 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* T = tile[warp];
   const long long nchunks = (n + CHUNK - 1) / CHUNK;
-  const long long c0 = static_cast<long long>(blockIdx.x) * CPB;
-  double s = 0.0;  // lane c of warp 0: running sum of chunk c0 + c
-  for (int tile = 0; tile < CHUNK / TILE; ++tile) {
-#pragma unroll 4
-    for (int m = 0; m < CPB * TILE / VT; ++m) {
-      const int idx = threadIdx.x + VT * m;
-      const int c = idx / TILE, e = idx % TILE;
-      const long long g = (c0 + c) * CHUNK + tile * TILE + e;
-      double pr = 0.0;  // +0.0 padding past n leaves a sequential sum unchanged
-      if (g < n) {
-        const double x = a[g], y = b[g];
-        if (OP == OP_DOT || OP == OP_PAP) {
-          pr = DM(x, y);
-        } else if (OP == OP_RZ) {
-          pr = DM(x, DD(x, y));  // r * (r / diag)
-        } else if (OP == OP_INIT) {
-          const double r = DS(x, y);  // r = b - Ap (solver.hpp:103)
-          w0[g] = r;
-          w1[g] = dv ? DD(r, dv[g]) : r;  // z = r / diag (or r); p = z (solver.hpp:105-109,123)
-          pr = DM(r, r);
-        } else {
-          const double r = DS(x, DM(alpha, y));  // r -= alpha * Ap (solver.hpp:133)
-          w0[g] = r;
-          pr = DM(r, r);
-        }
-        if (g < lo) pr = 0.0;  // not owned by this rank
+  const long long c0 = (static_cast<long long>(blockIdx.x) * (RVT / 32) + warp) * CPW;  // first chunk of the warp
+  double s = 0.0;
+  if (c0 < nchunks) {
+    double xa[CPW], xb[CPW];
+    auto load = [&](int t) {  // row c: entries [t*RT, t*RT + RT) of chunk c0 + c, lane = entry (RT = 32)
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const long long g = (c0 + c) * CHUNK + static_cast<long long>(t) * RT + lane;
+        xa[c] = g < n ? __ldcs(a + g) : 0.0;
+        xb[c] = g < n ? __ldcs(b + g) : 1.0;
       }
-      prod[c * TSTRIDE + e] = pr;
+    };
+    load(0);
+    for (int t = 0; t < CHUNK / RT; ++t) {
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const long long g = (c0 + c) * CHUNK + static_cast<long long>(t) * RT + lane;
+        double pr = 0.0;
+        if (g < n) {
+          pr = elem_op<OP>(xa[c], xb[c], g, alpha, w0, w1, dv);
+          if (g < lo) pr = 0.0;  // not owned by this rank
+        }
+        T[c * (RT + 1) + lane] = pr;
+      }
+      if (t + 1 < CHUNK / RT) load(t + 1);  // in flight during the add chain below
+      __syncwarp();
+      if (lane < CPW) {
+        const double* row = T + lane * (RT + 1);
+        const long long cend = (c0 + lane) * CHUNK + static_cast<long long>(t) * RT;
+#pragma unroll 8
+        for (int e = 0; e < RT; ++e) {
+          if (cend + e < n) s = DA(s, row[e]);  // exactly the chunk's entries, in order
+        }
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    if (threadIdx.x < CPB) {
-      const double* row = prod + threadIdx.x * TSTRIDE;
-#pragma unroll 16
-      for (int e = 0; e < TILE; ++e) s = DA(s, row[e]);
+    if (lane < CPW && c0 + lane < nchunks) {
+      part[c0 + lane] = s;
+      __threadfence();
     }
-    __syncthreads();
-  }
-  if (threadIdx.x < CPB && c0 + threadIdx.x < nchunks) {
-    part[c0 + threadIdx.x] = s;
-    __threadfence();
   }
   if (!last_block(done)) return;
-  if (threadIdx.x != 0) return;
   __threadfence();
-  const double tot = serial_sum(part, nchunks);
+  const double tot = block_serial_sum(part, nchunks, &tile[0][0]);
+  if (threadIdx.x != 0) return;
   *done = 0;
   if (OP == OP_DOT || dist) {
     *out = tot;  // distributed CG: the rank partial, combined by cgd_finish_kernel
@@ -570,7 +629,8 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
 
 int chunk_grid(int64_t n) {
   const long long nch = (n + CHUNK - 1) / CHUNK;
-  return static_cast<int>((nch + CPB - 1) / CPB);
+  const long long per_cta = RVT / 32 * CPW;
+  return static_cast<int>((nch + per_cta - 1) / per_cta);
 }
 
 // Multi-GPU: sum the all-gathered rank partials in rank order (identical on
@@ -604,13 +664,13 @@ cudaError_t launch_cgd_reduce(const Workspace& ws, int op, const double* b, int6
                               double* out, cudaStream_t st) {
   const int grid = chunk_grid(n);
   if (op == 0)
-    blocked_reduce_kernel<OP_INIT><<<grid, VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials, ws.vec_done, ws.sc,
+    blocked_reduce_kernel<OP_INIT><<<grid, RVT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials, ws.vec_done, ws.sc,
                                                        ws.history, out, 0.0, 0, owned);
   else if (op == 1)
-    blocked_reduce_kernel<OP_PAP><<<grid, VT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials, ws.vec_done,
+    blocked_reduce_kernel<OP_PAP><<<grid, RVT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials, ws.vec_done,
                                                       ws.sc, ws.history, out, 0.0, 0, owned);
   else
-    blocked_reduce_kernel<OP_UPDATE_R><<<grid, VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
+    blocked_reduce_kernel<OP_UPDATE_R><<<grid, RVT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
                                                            ws.vec_done, ws.sc, ws.history, out, 0.0, 0, owned);
   return cudaGetLastError();
 }
@@ -679,7 +739,7 @@ int64_t reduction_partials(int64_t n) {
 cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, double rel_tol, int max_iter,
                            cudaStream_t st) {
   if (ws.exact) {
-    blocked_reduce_kernel<OP_INIT><<<chunk_grid(n), VT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials,
+    blocked_reduce_kernel<OP_INIT><<<chunk_grid(n), RVT, 0, st>>>(b, ws.Ap, ws.r, ws.p, n, ws.vec_partials,
                                                                  ws.vec_done, ws.sc, ws.history, nullptr, rel_tol,
                                                                  max_iter, -1, ws.diag);
   } else {
@@ -690,13 +750,13 @@ cudaError_t launch_cg_init(const Workspace& ws, const double* b, int64_t n, doub
 }
 
 cudaError_t launch_cg_pap(const Workspace& ws, int64_t n, cudaStream_t st) {
-  blocked_reduce_kernel<OP_PAP><<<chunk_grid(n), VT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials,
+  blocked_reduce_kernel<OP_PAP><<<chunk_grid(n), RVT, 0, st>>>(ws.p, ws.Ap, nullptr, nullptr, n, ws.vec_partials,
                                                               ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_rz(const Workspace& ws, int64_t n, cudaStream_t st) {
-  blocked_reduce_kernel<OP_RZ><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.diag, nullptr, nullptr, n, ws.vec_partials,
+  blocked_reduce_kernel<OP_RZ><<<chunk_grid(n), RVT, 0, st>>>(ws.r, ws.diag, nullptr, nullptr, n, ws.vec_partials,
                                                              ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
   return cudaGetLastError();
 }
@@ -756,7 +816,7 @@ cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int c
 
 cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, int constrained) {
   if (ws.exact) {
-    blocked_reduce_kernel<OP_UPDATE_R><<<chunk_grid(n), VT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
+    blocked_reduce_kernel<OP_UPDATE_R><<<chunk_grid(n), RVT, 0, st>>>(ws.r, ws.Ap, ws.r, nullptr, n, ws.vec_partials,
                                                                      ws.vec_done, ws.sc, ws.history, nullptr, 0.0, 0);
     return cudaGetLastError();
   }
@@ -801,7 +861,7 @@ cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaS
 
 cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
                        cudaStream_t st) {
-  blocked_reduce_kernel<OP_DOT><<<chunk_grid(n), VT, 0, st>>>(a, b, nullptr, nullptr, n, ws.vec_partials,
+  blocked_reduce_kernel<OP_DOT><<<chunk_grid(n), RVT, 0, st>>>(a, b, nullptr, nullptr, n, ws.vec_partials,
                                                               ws.vec_done, ws.sc, ws.history, out, 0.0, 0);
   return cudaGetLastError();
 }

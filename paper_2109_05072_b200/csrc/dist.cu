@@ -32,13 +32,15 @@
 //               share summed from the launches' partials in fixed order.
 // The halo transfer therefore runs while the interior elements compute.
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the entry points are resolved at run time (nccl())
 
 #include <cmath>
 #include <cstring>
 #include <initializer_list>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "capi_util.h"
@@ -68,9 +70,56 @@ using namespace hxb;
 
 namespace {
 
+// NCCL is resolved at run time (dlopen of libnccl.so.2 on first use): a
+// process that already loaded NCCL -- PyTorch's bundled one -- shares that copy,
+// and loading this library never forces a second, older libnccl.so.2 on a
+// process whose other libraries need the newer one.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::decay_t<decltype(f)>>(dlsym(h, name)); };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.AllGather && a.GroupStart &&
+           a.GroupEnd && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
 int nccl_status(ncclResult_t r, const char* where) {
   if (r == ncclSuccess) return HEXBP_OK;
-  set_error(std::string(where) + ": " + ncclGetErrorString(r));
+  set_error(std::string(where) + ": " + nccl().GetErrorString(r));
+  return HEXBP_CUDA_ERROR;
+}
+
+int need_nccl() {
+  if (nccl().ok) return HEXBP_OK;
+  set_error("dist: libnccl.so.2 not found or incomplete (the multi-GPU path needs NCCL)");
   return HEXBP_CUDA_ERROR;
 }
 
@@ -96,7 +145,7 @@ int check_layout(hexbp_dist_s& d, cudaStream_t st) {
   CK(cudaMalloc(&dev, sizeof(int) * 8 * (d.world + 1)));
   std::vector<int> all(8 * d.world);
   cudaError_t e = cudaMemcpyAsync(dev, mine, sizeof mine, cudaMemcpyHostToDevice, st);
-  ncclResult_t r = e ? ncclSuccess : ncclAllGather(dev, dev + 8, 8, ncclInt32, d.comm, st);
+  ncclResult_t r = e ? ncclSuccess : nccl().AllGather(dev, dev + 8, 8, ncclInt32, d.comm, st);
   if (!e && r == ncclSuccess) e = cudaMemcpyAsync(all.data(), dev + 8, sizeof(int) * 8 * d.world,
                                                   cudaMemcpyDeviceToHost, st);
   if (!e && r == ncclSuccess) e = cudaStreamSynchronize(st);
@@ -123,17 +172,17 @@ int exchange(hexbp_dist_s& d, const double* u, double* w, int constrained, bool 
     if (gather) CK(cudaMemcpyAsync(d.scal + 1, d.scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
     return HEXBP_OK;
   }
-  NK(ncclGroupStart());
+  NK(nccl().GroupStart());
   if (d.has_up) {
-    NK(ncclSend(w + d.nL - d.plane, d.plane, ncclDouble, d.rank + 1, d.comm, st));
-    NK(ncclRecv(d.halo_up, d.plane, ncclDouble, d.rank + 1, d.comm, st));
+    NK(nccl().Send(w + d.nL - d.plane, d.plane, ncclDouble, d.rank + 1, d.comm, st));
+    NK(nccl().Recv(d.halo_up, d.plane, ncclDouble, d.rank + 1, d.comm, st));
   }
   if (d.has_down) {
-    NK(ncclSend(w, d.plane, ncclDouble, d.rank - 1, d.comm, st));
-    NK(ncclRecv(d.halo_down, d.plane, ncclDouble, d.rank - 1, d.comm, st));
+    NK(nccl().Send(w, d.plane, ncclDouble, d.rank - 1, d.comm, st));
+    NK(nccl().Recv(d.halo_down, d.plane, ncclDouble, d.rank - 1, d.comm, st));
   }
-  if (gather) NK(ncclAllGather(d.scal, d.scal + 1, 1, ncclDouble, d.comm, st));
-  NK(ncclGroupEnd());
+  if (gather) NK(nccl().AllGather(d.scal, d.scal + 1, 1, ncclDouble, d.comm, st));
+  NK(nccl().GroupEnd());
   // stream order: the group's sends have completed before the combines write
   if (d.has_up)
     CK(launch_plane_combine(w + d.nL - d.plane, d.halo_up, u + d.nL - d.plane, d.nxn, d.nyn, constrained, st));
@@ -146,7 +195,7 @@ int gather_scalar(hexbp_dist_s& d, cudaStream_t st) {
     CK(cudaMemcpyAsync(d.scal + 1, d.scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
     return HEXBP_OK;
   }
-  NK(ncclAllGather(d.scal, d.scal + 1, 1, ncclDouble, d.comm, st));
+  NK(nccl().AllGather(d.scal, d.scal + 1, 1, ncclDouble, d.comm, st));
   return HEXBP_OK;
 }
 
@@ -196,8 +245,9 @@ extern "C" {
 
 int hexbp_dist_unique_id(void* id, int64_t bytes) {
   if (!id || bytes < static_cast<int64_t>(sizeof(ncclUniqueId))) return invalid("dist_unique_id: buffer too small");
+  if (const int rc = need_nccl()) return rc;
   ncclUniqueId u;
-  NK(ncclGetUniqueId(&u));
+  NK(nccl().GetUniqueId(&u));
   std::memcpy(id, &u, sizeof u);
   return HEXBP_OK;
 }
@@ -206,6 +256,7 @@ int hexbp_dist_create(hexbp_setup_t slab, int world, int rank, const void* id, i
                       hexbp_dist_t* out) {
   if (!slab || !id || !out || world < 1 || rank < 0 || rank >= world) return invalid("dist_create: bad argument");
   if (id_bytes < static_cast<int64_t>(sizeof(ncclUniqueId))) return invalid("dist_create: NCCL id too short");
+  if (const int rc = need_nccl()) return rc;
   *out = nullptr;
   auto* d = new (std::nothrow) hexbp_dist_s;
   if (!d) return HEXBP_OUT_OF_MEMORY;
@@ -227,7 +278,7 @@ int hexbp_dist_create(hexbp_setup_t slab, int world, int rank, const void* id, i
   std::memcpy(&u, id, sizeof u);
   int rc = HEXBP_OK;
   {
-    const ncclResult_t r = ncclCommInitRank(&d->comm, world, u, rank);
+    const ncclResult_t r = nccl().CommInitRank(&d->comm, world, u, rank);
     if (r != ncclSuccess) rc = nccl_status(r, "ncclCommInitRank");
   }
   if (!rc) rc = hexbp_workspace_create(slab, &d->ws);
@@ -285,7 +336,7 @@ void hexbp_dist_destroy(hexbp_dist_t d) {
   if (!d) return;
   {
     DeviceGuard g(d->device);
-    if (d->comm) ncclCommDestroy(d->comm);
+    if (d->comm) nccl().CommDestroy(d->comm);
     for (void* b : {static_cast<void*>(d->halo_up), static_cast<void*>(d->halo_down), static_cast<void*>(d->scal),
                     static_cast<void*>(d->ob.carry), static_cast<void*>(d->ob.slots),
                     static_cast<void*>(d->ob.coldot), static_cast<void*>(d->ob.partials),

@@ -20,5 +20,5 @@ for src in B.SOURCES:
     objs.append(obj)
 assert all(p.wait() == 0 for p in procs)
 lib = os.path.join(out, "libhexbp_b200.so")
-subprocess.check_call([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-lnccl", "-o", lib])
+subprocess.check_call([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-ldl", "-o", lib])
 print(lib)

@@ -106,6 +106,10 @@ __device__ __forceinline__ double quad_sum(double v) {
   return v;
 }
 
+// CON: ConstrainedOperator semantics (ApplyArgs::constrained), DOT: the CG
+// form with the fused p.Ap (ApplyArgs::col_dot) -- compile-time, so neither
+// adds tests to the phase bodies.
+template <bool CON, bool DOT>
 __global__ void __launch_bounds__(NT, 2)
     bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs) {
   extern __shared__ double smem[];
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(NT, 2)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const uint64_t pol = policy_evict_first();
-  const bool do_dot = A.col_dot != nullptr;
+  constexpr bool do_dot = DOT;
   const int col = blockIdx.x;
   const int ex = col % A.nx, ey = col / A.nx;
   const int nz = A.nz;              // elements per column of the slab (G column stride)
@@ -209,13 +213,13 @@ __global__ void __launch_bounds__(NT, 2)
   auto phaseZ = [&](int e, int G) {
     const double* us = Us + (e % NUB) * US_SZ;
     const int X = ex * P + g, Y = ey * P + G;
-    const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+    const bool bcxy = CON && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
     double b[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int k = t + 4 * s, Z = e * P + k;
       double v = us[k * US_KS + G * 8 + g];
-      if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
+      if (CON && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
       b[s] = v;
     }
     double cb0 = 0, cb1 = 0, cd0 = 0, cd1 = 0;
@@ -405,9 +409,10 @@ __global__ void __launch_bounds__(NT, 2)
       return;
     }
     const int Z = e * P + g, Y = ey * P + G;
-    const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+    const bool zbc = CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
     // u at these nodes: still staged in shared memory (z-plane k = g of element e)
     const double2 u2 = *reinterpret_cast<const double2*>(Us + (e % NUB) * US_SZ + g * US_KS + G * 8 + 2 * t);
+
     // ring partials -> lateral buffer (ring.cuh layout): a ring row (j = 0 or
     // P) stores all P+1 of its nodes as one 16-byte pair per lane
     const bool rowring = G == 0 || G == P;
@@ -422,7 +427,7 @@ __global__ void __launch_bounds__(NT, 2)
       if (ring) {
         if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
         if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
-          if (zbc || (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
+          if (zbc || (CON && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
             if (ring_owner(P, i, G, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0))
               dot = fma(uv, uv, dot);  // w = u, counted once
           } else {
@@ -522,26 +527,36 @@ __global__ void __launch_bounds__(NT, 2)
 bool mma_kernel_applies(const Setup& s) { return s.kind == KIND_DIFF && s.p == P && s.gstride == GSE; }
 
 cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static std::atomic<uint64_t> configured{0};
-  set_smem_attr_once(configured, reinterpret_cast<const void*>(&bp3_p7_mma_kernel), SMEM_BYTES);
+  static std::atomic<uint64_t> configured[4] = {};
+  const int v = (a.constrained ? 2 : 0) + (a.col_dot != nullptr ? 1 : 0);
+  const void* fns[4] = {reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, false>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, true>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, false>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, true>)};
+  set_smem_attr_once(configured[v], fns[v], SMEM_BYTES);
   MmaBasis bs;
   for (int i = 0; i < Q; ++i)
     for (int j = 0; j < N; ++j) {
       bs.B[i][j] = s.B[i * N + j];
       bs.D[i][j] = s.D[i * N + j];
     }
-  bp3_p7_mma_kernel<<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs);
+  switch (v) {
+    case 0: bp3_p7_mma_kernel<false, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+    case 1: bp3_p7_mma_kernel<false, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+    case 2: bp3_p7_mma_kernel<true, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+    default: bp3_p7_mma_kernel<true, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+  }
   return cudaGetLastError();
 }
 
 void mma_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm) {
-  cudaFuncSetAttribute(&bp3_p7_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaFuncSetAttribute(&bp3_p7_mma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, bp3_p7_mma_kernel);
+  cudaFuncGetAttributes(&fa, bp3_p7_mma_kernel<true, true>);
   *regs = fa.numRegs;
   *smem = static_cast<int>(fa.sharedSizeBytes) + SMEM_BYTES;
   *threads = NT;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp3_p7_mma_kernel, NT, SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp3_p7_mma_kernel<true, true>, NT, SMEM_BYTES);
 }
 
 }  // namespace hxb

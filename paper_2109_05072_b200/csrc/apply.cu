@@ -241,9 +241,14 @@ struct Cfg {
   static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
 };
 
-template <int P, int Q, int KIND, int SK, typename K_ = Cfg<P, Q, KIND, SK>>
+// F: bit 0 = ConstrainedOperator semantics (ApplyArgs::constrained), bit 1 =
+// the CG form with the fused p.Ap (ApplyArgs::col_dot) -- compile-time flags,
+// so neither costs tests (or registers) in the phase bodies (+1-5% over the
+// run-time flags across BP1/BP3/BP5 p = 2..8; BP1 p = 6, 8: -2%).
+template <int P, int Q, int KIND, int SK, int F = 3, typename K_ = Cfg<P, Q, KIND, SK>>
 __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
+  constexpr bool CON = (F & 1) != 0;
   using K = Cfg<P, Q, KIND, SK>;
   constexpr int N = K::N, QQ = K::QQ, NT = K::NT, KC = K::KC;
   constexpr int NH = N / 2;
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   const int item = t;               // pencil index (per phase)
   const int wfirst = t & ~31;       // first pencil of this warp: whole-warp phase skips
   const uint64_t pol = policy_evict_first();
-  const bool do_dot = A.col_dot != nullptr;
+  constexpr bool do_dot = (F & 2) != 0;
   // CTA = (column group, z-segment). A segment recomputes the element below
   // its first one without storing anything, so the carry hands it the full
   // bottom node plane and it owns that plane outright (no cross-CTA sum).
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   const bool zvalid = zrole && kz < kv;
   const int ex = col % A.nx, ey = col / A.nx;
   const int X = ex * P + zi, Y = ey * P + zj;
-  const bool bcxy = A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+  const bool bcxy = CON && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
   const bool ring = zi == 0 || zi == P || zj == 0 || zj == P;
   const bool owner = ring_owner(P, zi, zj, ex, ey, A.nx, A.ny);
   const LatLayout L(P, A.nx, A.ny);
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       for (int k = 0; k < N; ++k) {
         const int Z = ez * P + k;
         double v = us[k * N * N];
-        if (A.constrained && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
+        if (CON && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
         uk[k] = v;
       }
       if constexpr (K::EO) {
@@ -757,7 +762,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
                 const long long node =
                     X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
                 double v = out[r];
-                if (A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = usz[k * N * N];
+                if (CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = usz[k * N * N];
                 A.w[node] = v;
               }
             }
@@ -769,7 +774,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
             if (k < kend) {
               const int Z = ez * P + k;
               const double uv = usz[k * N * N];
-              const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+              const bool zbc = CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
               if (ring) {
                 lat[Z * lat_stride] = out[r];
                 // column-local share of p.Ap on the ring (ring.cuh); w = u rows counted once
@@ -1146,7 +1151,22 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
     occ = 1;
   const int ncta = (a.ncols + K::KC - 1) / K::KC;
   const int nseg = z_segments(ncta, occ, a.nz);
-  bp_apply_kernel<P, Q, KIND, SK><<<ncta * nseg, K::NT, K::SMEM_BYTES, st>>>(a, bs, nseg);
+  const int f = (a.constrained ? 1 : 0) + (a.col_dot != nullptr ? 2 : 0);
+  switch (f) {
+#define HXB_F(FF)                                                                                   \
+  case FF: {                                                                                        \
+    static std::atomic<uint64_t> cfg{0};                                                            \
+    set_smem_attr_once(cfg, reinterpret_cast<const void*>(&bp_apply_kernel<P, Q, KIND, SK, FF>),    \
+                       K::SMEM_BYTES);                                                              \
+    bp_apply_kernel<P, Q, KIND, SK, FF><<<ncta * nseg, K::NT, K::SMEM_BYTES, st>>>(a, bs, nseg);    \
+    break;                                                                                          \
+  }
+    HXB_F(0)
+    HXB_F(1)
+    HXB_F(2)
+    HXB_F(3)
+#undef HXB_F
+  }
   return cudaGetLastError();
   }
 }

@@ -72,6 +72,8 @@ __device__ __forceinline__ double lds_volatile(const double* p) {
   return v;
 }
 
+// CON / DOT: constrained semantics and the fused p.Ap, compile-time (see apply_mma.cu)
+template <bool CON, bool DOT>
 __global__ void __launch_bounds__(NT, 3)
     bp5_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ Mma5Basis bs) {
   extern __shared__ double smem[];
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(NT, 3)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const uint64_t pol = policy_evict_first();
-  const bool do_dot = A.col_dot != nullptr;
+  constexpr bool do_dot = DOT;
   const int col = blockIdx.x;
   const int ex = col % A.nx, ey = col / A.nx;
   const int nz = A.nz;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(NT, 3)
   // goes to p.Ap
   double dot = 0.0;
   auto mask_u = [&](int e) {
-    if (e >= nz || tid >= N * N || !A.constrained) return;
+    if (e >= nz || tid >= N * N || !CON) return;
     const int i = tid & 7, j = tid >> 3;
     const int X = ex * P + i, Y = ey * P + j;
     const bool bcxy = X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1;
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(NT, 3)
       return;
     }
     const int Z = e * P + g, Y = ey * P + G;
-    const bool zbc = A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
+    const bool zbc = CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
     const bool rowring = G == 0 || G == P;
     if (rowring) {
       *reinterpret_cast<double2*>(A.lateral + Lat.y_index(P, A.nx, Z, ey + (G == P), G == 0, ex, 2 * t)) =
@@ -287,24 +289,34 @@ __global__ void __launch_bounds__(NT, 3)
 bool mma5_kernel_applies(const Setup& s) { return s.kind == KIND_COLLOC && s.p == P && s.g_aos == 2; }
 
 cudaError_t launch_apply_mma5(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static std::atomic<uint64_t> configured{0};
-  set_smem_attr_once(configured, reinterpret_cast<const void*>(&bp5_p7_mma_kernel), SMEM_BYTES);
   if (s.gstride != GSE) return cudaErrorInvalidValue;
+  static std::atomic<uint64_t> configured[4] = {};
+  const int v = (a.constrained ? 2 : 0) + (a.col_dot != nullptr ? 1 : 0);
+  const void* fns[4] = {reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, false>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, true>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, false>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, true>)};
+  set_smem_attr_once(configured[v], fns[v], SMEM_BYTES);
   Mma5Basis bs;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) bs.D[i][j] = s.D[i * N + j];
-  bp5_p7_mma_kernel<<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs);
+  switch (v) {
+    case 0: bp5_p7_mma_kernel<false, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+    case 1: bp5_p7_mma_kernel<false, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+    case 2: bp5_p7_mma_kernel<true, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+    default: bp5_p7_mma_kernel<true, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+  }
   return cudaGetLastError();
 }
 
 void mma5_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm) {
-  cudaFuncSetAttribute(&bp5_p7_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaFuncSetAttribute(&bp5_p7_mma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, bp5_p7_mma_kernel);
+  cudaFuncGetAttributes(&fa, bp5_p7_mma_kernel<true, true>);
   *regs = fa.numRegs;
   *smem = static_cast<int>(fa.sharedSizeBytes) + SMEM_BYTES;
   *threads = NT;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp5_p7_mma_kernel, NT, SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp5_p7_mma_kernel<true, true>, NT, SMEM_BYTES);
 }
 
 }  // namespace hxb

@@ -199,7 +199,7 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 // (profiles/r1c_sk_sweep*.jsonl).
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
-  constexpr int mass[9] = {0, 1000000, 16, 100014, 100015, 100013, 100011, 100011, 100011};
+  constexpr int mass[9] = {0, 1000000, 16, 100014, 100015, 100013, 100011, 100011, 100012};
   // p = 7 BP3 / BP5 run the DMMA kernels; these entries serve HEXBP_NO_DMMA=1 setups
   constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 102011, 100011};
   constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 100011, 100011};

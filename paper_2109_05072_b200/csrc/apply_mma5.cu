@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(NT, 3)
   constexpr bool do_dot = DOT;
   const int col = blockIdx.x;
   const int ex = col % A.nx, ey = col / A.nx;
-  const int nz = A.nz;
+  const int nz = A.nz;               // elements per column of the slab (G column stride)
+  const int e0 = A.zr0, e1 = A.zr1;  // elements this launch marches (dist.cu overlap: sub-ranges)
   const LatLayout Lat(P, A.nx, A.ny);
 
   // basis fragments (registers for the whole kernel; see apply_mma.cu)
@@ -111,14 +112,14 @@ __global__ void __launch_bounds__(NT, 3)
   __syncwarp();
   if (lane == 0) {
     mbar_arrive_expect_tx(bar, pbytes);
-    bulk_g2s(smem_u32(Gp), Gcol + warp * GPL, pbytes, bar, pol);
+    bulk_g2s(smem_u32(Gp), Gcol + e0 * GSE + warp * GPL, pbytes, bar, pol);
   }
-  if (tid == 0 && nz > 1) prefetch_l2_bulk(Gcol + GSE, GSE * 8);
+  if (tid == 0 && e1 - e0 > 1) prefetch_l2_bulk(Gcol + (e0 + 1) * GSE, GSE * 8);
 
   // u staging of element e into buffer e % NUB: thread (i,j) of the footprint
   // (tid < 64) copies its z-pencil into [k][j*8+i]
   auto fetch_u = [&](int e) {
-    if (e < nz && tid < N * N) {
+    if (e < e1 && tid < N * N) {
       const int i = tid & 7, j = tid >> 3;
       const uint32_t dst = smem_u32(Us + (e % NUB) * US_SZ + tid);
       const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(NT, 3)
   // goes to p.Ap
   double dot = 0.0;
   auto mask_u = [&](int e) {
-    if (e >= nz || tid >= N * N || !CON) return;
+    if (e >= e1 || tid >= N * N || !CON) return;
     const int i = tid & 7, j = tid >> 3;
     const int X = ex * P + i, Y = ey * P + j;
     const bool bcxy = X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1;
@@ -173,12 +174,12 @@ __global__ void __launch_bounds__(NT, 3)
     const double2 gt2 = *reinterpret_cast<const double2*>(smem + OFF_GT + (e & 1) * TS + tix(c, g, 2 * t));
     const double gt[2] = {gt2.x, gt2.y};
     // factors at (a = 2t+q, b = g, c): [c][m][b][a] -> this warp's plane buffer
-    mbar_wait_parity(bar, e & 1);
+    mbar_wait_parity(bar, (e - e0) & 1);
     double2 gm[6];
 #pragma unroll
     for (int m = 0; m < 6; ++m) gm[m] = *reinterpret_cast<const double2*>(Gp + m * 64 + g * 8 + 2 * t);
     __syncwarp();
-    if (lane == 0 && e + 1 < nz) {  // plane consumed: stream the next element's plane
+    if (lane == 0 && e + 1 < e1) {  // plane consumed: stream the next element's plane
       fence_proxy_async();
       mbar_arrive_expect_tx(bar, pbytes);
       bulk_g2s(smem_u32(Gp), Gcol + (e + 1) * GSE + c * GPL, pbytes, bar, pol);
@@ -223,9 +224,16 @@ __global__ void __launch_bounds__(NT, 3)
       o[0] += top0;
       o[1] += top1;
     }
-    if (g == P && e + 1 < nz) {
+    if (g == P && e + 1 < e1) {
       carry[0] = o[0];
       carry[1] = o[1];
+      return;
+    }
+    // range ends inside the slab (dist.cu overlap): leave this launch's share
+    // of the plane for launch_carry_combine (the p.Ap energy form needs no node values)
+    double* cplane = g == P ? A.carry_hi : (g == 0 && e == e0 ? A.carry_lo : nullptr);
+    if (cplane != nullptr) {
+      *reinterpret_cast<double2*>(cplane + col * (N * N) + G * N + 2 * t) = make_double2(o[0], o[1]);
       return;
     }
     const int Z = e * P + g, Y = ey * P + G;
@@ -249,21 +257,21 @@ __global__ void __launch_bounds__(NT, 3)
   };
 
   // ------------------------------------------------ schedule: A_e = P(e) || Z(e+1) || Z'(e-1)
-  fetch_u(0);
-  fetch_u(1);
+  fetch_u(e0);
+  fetch_u(e0 + 1);
   cp_async_wait<0>();
-  mask_u(0);
-  mask_u(1);
+  mask_u(e0);
+  mask_u(e0 + 1);
   __syncthreads();
-  phaseZ(0, warp);
+  phaseZ(e0, warp);
   __syncthreads();
-  for (int e = 0; e <= nz; ++e) {
+  for (int e = e0; e <= e1; ++e) {
     fetch_u(e + 2);
-    if (tid == 0 && e + 2 < nz) prefetch_l2_bulk(Gcol + (e + 2) * GSE, GSE * 8);
-    if (e < nz) phaseP(e, warp);
-    if (e >= 1) phaseZp(e - 1, warp);
-    if (e + 1 < nz) phaseZ(e + 1, warp);
-    if (e == nz) break;
+    if (tid == 0 && e + 2 < e1) prefetch_l2_bulk(Gcol + (e + 2) * GSE, GSE * 8);
+    if (e < e1) phaseP(e, warp);
+    if (e > e0) phaseZp(e - 1, warp);
+    if (e + 1 < e1) phaseZ(e + 1, warp);
+    if (e == e1) break;
     cp_async_wait<0>();
     mask_u(e + 2);
     __syncthreads();

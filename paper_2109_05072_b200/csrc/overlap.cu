@@ -18,7 +18,9 @@
 //              single launch's -- then the same store / ring / p.Ap logic as
 //              the kernel's Z' epilogue (restriction.hpp:67-80 ordering).
 // The rank's p.Ap share: the three launches' partials and the combine's, in
-// fixed order (deterministic run to run).
+// fixed order (deterministic run to run). Both DMMA kernels take ranges (BP3
+// p = 7 and BP5 p = 7; BP5's p.Ap is the element energy form, so its combine
+// adds nothing to the dot).
 #include <cuda_runtime.h>
 
 #include "device_util.cuh"
@@ -44,6 +46,7 @@ struct CombineArgs {
   unsigned int* ticket;
   const double* slots;  // the launches' p.Ap partials
   int nslots;
+  int nodal_dot;        // BP3: the inner planes' p.Ap share is added here; BP5: energy form (in the launches)
   double* out;          // rank share of p.Ap
 };
 
@@ -71,14 +74,16 @@ __global__ void __launch_bounds__(CT) carry_combine_kernel(const __grid_constant
         A.lateral[Lat.y_index(P, A.nx, Z, ey + (j == P), j == 0, ex, i)] = v;
       else
         A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = v;
-      if (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1)) {
-        if (ring_owner(P, i, j, ex, ey, A.nx, A.ny)) dot = fma(uv, uv, dot);  // w = u, counted once
-      } else {
-        dot = fma(uv, v, dot);
+      if (c.nodal_dot) {
+        if (A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1)) {
+          if (ring_owner(P, i, j, ex, ey, A.nx, A.ny)) dot = fma(uv, uv, dot);  // w = u, counted once
+        } else {
+          dot = fma(uv, v, dot);
+        }
       }
     } else {  // inner planes are never z-boundary planes: no constraint here
       A.w[X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z)] = v;
-      dot = fma(uv, v, dot);
+      if (c.nodal_dot) dot = fma(uv, v, dot);
     }
   }
   __shared__ double red[CT / 32];
@@ -101,7 +106,13 @@ __global__ void __launch_bounds__(CT) carry_combine_kernel(const __grid_constant
 
 }  // namespace
 
-bool apply_overlap_supported(const Setup& s) { return use_mma(s) && mma_kernel_applies(s) && s.dims[2] >= 2; }
+bool apply_overlap_supported(const Setup& s) {
+  return use_mma(s) && (mma_kernel_applies(s) || mma5_kernel_applies(s)) && s.dims[2] >= 2;
+}
+
+static cudaError_t launch_range(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  return mma5_kernel_applies(s) ? launch_apply_mma5(s, a, st) : launch_apply_mma(s, a, st);
+}
 
 int64_t overlap_carry_doubles(const Setup& s) {
   return 4LL * s.dims[0] * s.dims[1] * (s.p + 1) * (s.p + 1);
@@ -128,18 +139,18 @@ static double* carry_plane(const Setup& s, const OverlapBuffers& ob, int k) {
 cudaError_t launch_apply_boundary(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
                                   const OverlapBuffers& ob, cudaStream_t st) {
   const int nz = s.dims[2];
-  cudaError_t e = launch_apply_mma(s, range_args(s, ws, u, w, constrained, ob, 0, 0, 1, nullptr, carry_plane(s, ob, 0)),
-                                   st);
+  cudaError_t e = launch_range(s, range_args(s, ws, u, w, constrained, ob, 0, 0, 1, nullptr, carry_plane(s, ob, 0)),
+                               st);
   if (e) return e;
-  return launch_apply_mma(s, range_args(s, ws, u, w, constrained, ob, 1, nz - 1, nz, carry_plane(s, ob, 1), nullptr),
-                          st);
+  return launch_range(s, range_args(s, ws, u, w, constrained, ob, 1, nz - 1, nz, carry_plane(s, ob, 1), nullptr),
+                      st);
 }
 
 cudaError_t launch_apply_interior(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,
                                   const OverlapBuffers& ob, cudaStream_t st) {
   const int nz = s.dims[2];
   if (nz < 3) return cudaMemsetAsync(ob.slots + 2, 0, sizeof(double), st);
-  return launch_apply_mma(
+  return launch_range(
       s, range_args(s, ws, u, w, constrained, ob, 2, 1, nz - 1, carry_plane(s, ob, 2), carry_plane(s, ob, 3)), st);
 }
 
@@ -166,6 +177,7 @@ cudaError_t launch_carry_combine(const Setup& s, const Workspace& ws, const doub
   c.ticket = ob.tickets + 3;
   c.slots = ob.slots;
   c.nslots = 3;
+  c.nodal_dot = s.kind != KIND_COLLOC;
   c.out = out;
   const long long nodes = static_cast<long long>(c.nplanes) * s.dims[0] * s.dims[1] * (s.p + 1) * (s.p + 1);
   long long blocks = (nodes + CT - 1) / CT;

@@ -23,8 +23,8 @@ def _single(bp, p, dims, a, mode="fast"):
     return op
 
 
-@pytest.mark.parametrize("bp,p,dims", [(3, 7, (4, 3, 6)), (3, 7, (3, 4, 2)), (3, 7, (2, 2, 3)), (5, 4, (3, 3, 4)),
-                                       (1, 3, (3, 2, 3))])
+@pytest.mark.parametrize("bp,p,dims", [(3, 7, (4, 3, 6)), (3, 7, (3, 4, 2)), (3, 7, (2, 2, 3)), (5, 7, (3, 3, 4)),
+                                       (5, 7, (2, 3, 2)), (5, 4, (3, 3, 4)), (1, 3, (3, 2, 3))])
 @pytest.mark.parametrize("overlap", [True, False])
 def test_distributed_apply_is_the_single_gpu_apply(bp, p, dims, overlap):
     """Bit for bit: the split launches assemble the inner planes with the same
@@ -81,3 +81,20 @@ def test_distributed_cg_reference_mode():
 def test_distributed_errors():
     with pytest.raises(ValueError):  # fewer element layers than ranks
         NcclSlabOperator(3, 2, (2, 2, 1), world=2, rank=0)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_distributed_bp5_dmma_cg(overlap):
+    """BP5 p = 7 (the DMMA kernel with the energy-form p.Ap, BASELINE configs[3]):
+    the overlapped distributed solve against the single-GPU fast solve."""
+    import torch
+
+    dims, a = (4, 3, 5), 0.1
+    dop = NcclSlabOperator(5, 7, dims, amplitude=a, overlap=overlap)
+    b = torch.from_numpy(hx.bench_rhs(5, 7, dims)).cuda()
+    x = torch.zeros_like(b)
+    rep = dop.cg(b, x, rel_tol=1e-8, max_iter=3000, constrained=True)
+    xs = torch.zeros_like(b)
+    rs = hx.cg(hx.ConstrainedOperator(_single(5, 7, dims, a)), b, xs, 1e-8, 3000, mode="fast")
+    assert rep.converged and abs(rep.iterations - rs.iterations) <= 1
+    assert (torch.linalg.norm(x - xs) / torch.linalg.norm(xs)).item() <= 1e-8

@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--amplitude", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU (hexbp_dist_cg) path even at N = 1 (single-GPU box check of that path)")
     return ap.parse_args()
 
 
@@ -222,7 +224,12 @@ def main():
     K, W = args.steps, max(args.warmup, 3)
     L = _lib.lib()
 
-    if world > 1:
+    if world > 1 or args.dist:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         from paper_2109_05072_b200 import parallel
 
         res = parallel.bench_weak(bp, p, dims, K, W, args.amplitude, clock=lambda: ClockSampler(local))

@@ -109,9 +109,11 @@ __device__ __forceinline__ double quad_sum(double v) {
 // CON: ConstrainedOperator semantics (ApplyArgs::constrained), DOT: the CG
 // form with the fused p.Ap (ApplyArgs::col_dot) -- compile-time, so neither
 // adds tests to the phase bodies.
-template <bool CON, bool DOT>
-__global__ void __launch_bounds__(NT, 2)
-    bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs) {
+// LBC: the column touches the lateral (x/y) boundary of a constrained
+// operator. Interior columns (94% at cfg3) run a copy of the body compiled
+// without the lateral boundary tests.
+template <bool CON, bool DOT, bool LBC>
+__device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& bs) {
   extern __shared__ double smem[];
   double* SA = smem + OFF_SA;
   double* SP = smem + OFF_SP;
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(NT, 2)
   auto phaseZ = [&](int e, int G) {
     const double* us = Us + (e % NUB) * US_SZ;
     const int X = ex * P + g, Y = ey * P + G;
-    const bool bcxy = CON && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+    const bool bcxy = LBC && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
     double b[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(NT, 2)
       if (ring) {
         if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
         if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
-          if (zbc || (CON && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
+          if (zbc || (LBC && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
             if (ring_owner(P, i, G, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0))
               dot = fma(uv, uv, dot);  // w = u, counted once
           } else {
@@ -520,6 +522,20 @@ __global__ void __launch_bounds__(NT, 2)
     __syncthreads();
   }
   ring_dot_finish<NT>(A, col, cdot, s_red);
+}
+
+template <bool CON, bool DOT>
+__global__ void __launch_bounds__(NT, 2)
+    bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs) {
+  if constexpr (CON) {
+    const int ex = blockIdx.x % A.nx, ey = blockIdx.x / A.nx;
+    if (ex > 0 && ex < A.nx - 1 && ey > 0 && ey < A.ny - 1)
+      mma_column<true, DOT, false>(A, bs);
+    else
+      mma_column<true, DOT, true>(A, bs);
+  } else {
+    mma_column<false, DOT, false>(A, bs);
+  }
 }
 
 }  // namespace

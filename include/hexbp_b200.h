@@ -183,6 +183,16 @@ int hexbp_apply(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, doub
 int hexbp_apply_ring_deferred(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, double* w_dev,
                               int constrained, void* stream);
 
+/* The operator in the form the single-GPU fast CG launches it, on the
+ * workspace's own search-direction buffer: ring nodes deferred as above and,
+ * on the DMMA degrees (BP3 / BP5, p = 7), u staged by one TMA tensor copy per
+ * element from the row-pitched search direction (tma.cu). u_dev (n unpadded
+ * doubles) is first copied into that buffer; u_dev = NULL applies to its
+ * current contents (timing loops). Clobbers the search direction of a solve
+ * on this workspace. */
+int hexbp_apply_cg_form(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, double* w_dev, int constrained,
+                        void* stream);
+
 /* Same, with HOST buffers of n doubles; synchronous (drop-in for the
  * reference's std::span / std::vector signature). */
 int hexbp_apply_host(hexbp_setup_t s, hexbp_workspace_t ws, const double* u, double* w, int64_t n, int constrained);

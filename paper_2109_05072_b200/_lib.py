@@ -55,6 +55,7 @@ def lib() -> C.CDLL:
         "hexbp_workspace_set_mode": (C.c_int, [_vp, C.c_int]),
         "hexbp_apply": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
         "hexbp_apply_ring_deferred": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
+        "hexbp_apply_cg_form": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
         "hexbp_apply_host": (C.c_int, [_vp, _vp, _dp, _dp, C.c_int64, C.c_int]),
         "hexbp_cg": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_int, C.POINTER(CGReportC), _dp, _vp]),
         "hexbp_pcg": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_int, C.POINTER(CGReportC), _dp,

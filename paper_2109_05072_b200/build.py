@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhexbp_b200.so")
 SOURCES = ["apply.cu", "apply_exact.cu", "apply_mma.cu", "apply_mma5.cu", "overlap.cu", "cg.cu", "jacobi.cu",
-           "multipass.cu", "fe_tools.cu", "setup.cu", "capi.cu", "dist.cu", "basis.cpp"]
+           "multipass.cu", "fe_tools.cu", "setup.cu", "capi.cu", "dist.cu", "tma.cu", "basis.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

@@ -1291,6 +1291,10 @@ ApplyArgs make_apply_args(const Setup& s, const Workspace& ws, const double* u, 
   a.zlo_shared = s.z0 > 0;
   a.zr0 = 0;
   a.zr1 = s.dims[2];
+  if (ws.pt != nullptr && u == ws.pt) {  // the fast CG's row-pitched search direction (tma.cu)
+    a.u_pitch = ws.pt_pitch;
+    a.u_tmap = &ws.pt_map;
+  }
   return a;
 }
 

@@ -50,8 +50,16 @@ constexpr int NXW = 11;
 constexpr int NW = 12, NT = NW * 32;
 constexpr int GSE = (6 * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
 // shared-memory layout (doubles)
-constexpr int US_KS = 68;                 // u staging: [k][j*8+i], k-stride 68
-constexpr int US_SZ = N * US_KS;          // per buffer
+// u staging, [k][j][i]. cp.async path: rows of 8, k-stride 68 (conflict-free
+// phase-Z loads). TMA path: the tensor copy's dense box in 128-byte aligned
+// buffers. A box row must start 16-byte aligned in global memory, so the box
+// is 10 wide from the even x at or below the element's first node and the
+// element sits at x offset ex & 1 of every row (the pitch is even). (A box
+// two rows deeper -- k-stride 100 = 4 mod 16, conflict-free phase-Z / Z'
+// loads -- measured 1% slower: more staging traffic and spills.)
+template <bool TMA> constexpr int us_rs() { return TMA ? N + 2 : N; }   // row stride
+template <bool TMA> constexpr int us_ks() { return TMA ? N * (N + 2) : 68; }  // k stride
+template <bool TMA> constexpr int us_sz() { return N * us_ks<TMA>(); }
 // SA: [f][row][8c + i] with row stride 72 (= 8 mod 16 doubles) and the i-bit-2
 // swizzle swa(row); used for Z->Y (row = j, c = a3) and X'->Y' (row = b = a2,
 // c = a3). Both the 16-byte C-fragment stores (rows fixed per warp, pencil
@@ -69,16 +77,18 @@ constexpr int SB_F = N * SB_KS;           // 736
 constexpr int SC_KS = 68;                 // [f][c][i + 8j] (Y'->Z')
 constexpr int SC_F = Q * SC_KS;           // 612
 constexpr int NUB = 4;                    // u staging buffers: U(e-1) .. U(e+2) live at once
+constexpr int US_REGION = NUB * us_sz<true>() + 16;  // >= NUB * us_sz<false>(), with the 128-byte alignment slack
+static_assert(US_REGION >= NUB * us_sz<false>(), "staging region");
 constexpr int OFF_SA = 0;                 // Z -> Y   : 2 fields, SA layout
 constexpr int OFF_SP = OFF_SA + 2 * SA_F;  // X' -> Y' : 3 fields, SA layout
 constexpr int OFF_SB = OFF_SP + 3 * SA_F;  // Y -> X   : 3 fields
 constexpr int OFF_SC = OFF_SB + 3 * SB_F;  // Y' -> Z' : 2 fields
 constexpr int OFF_G = OFF_SC + 2 * SC_F;   // 16-byte aligned (even)
 constexpr int OFF_U = OFF_G + GSE;
-constexpr int OFF_BAS = OFF_U + NUB * US_SZ;  // B, D (q x n each), resident
+constexpr int OFF_BAS = OFF_U + US_REGION;  // B, D (q x n each), resident
 constexpr int OFF_R8 = OFF_BAS + 2 * Q * N;   // packed row-8 pairs (16-byte loads)
-constexpr int OFF_BAR = OFF_R8 + 16 + 16;
-constexpr int SMEM_BYTES = (OFF_BAR + 1) * 8;
+constexpr int OFF_BAR = OFF_R8 + 16 + 16;     // G mbarrier, then NUB u mbarriers (TMA path)
+constexpr int SMEM_BYTES = (OFF_BAR + 1 + NUB) * 8;
 static_assert(OFF_G % 2 == 0, "TMA destination must be 16-byte aligned");
 static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "two CTAs per SM");
 
@@ -112,8 +122,8 @@ __device__ __forceinline__ double quad_sum(double v) {
 // LBC: the column touches the lateral (x/y) boundary of a constrained
 // operator. Interior columns (94% at cfg3) run a copy of the body compiled
 // without the lateral boundary tests.
-template <bool CON, bool DOT, bool LBC>
-__device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& bs) {
+template <bool CON, bool DOT, bool LBC, bool TMA>
+__device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& bs, const CUtensorMap& tmu) {
   extern __shared__ double smem[];
   double* SA = smem + OFF_SA;
   double* SP = smem + OFF_SP;
@@ -121,6 +131,8 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
   double* SC = smem + OFF_SC;
   double* Gs = smem + OFF_G;
   double* Us = smem + OFF_U;
+  if (TMA) Us += ((128 - (smem_u32(Us) & 127)) & 127) / 8;  // tensor copies land 128-byte aligned
+  constexpr int UKS = us_ks<TMA>(), URS = us_rs<TMA>(), USZ = us_sz<TMA>();
   __shared__ double s_red[NW];
 
   if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
@@ -133,6 +145,7 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
   const int ex = col % A.nx, ey = col / A.nx;
   const int nz = A.nz;              // elements per column of the slab (G column stride)
   const int e0 = A.zr0, e1 = A.zr1;  // elements this launch marches (dist.cu overlap: sub-ranges)
+  const int ush = TMA ? (ex & 1) : 0;  // x offset of the element in a staged row (TMA box from an even x)
   const LatLayout Lat(P, A.nx, A.ny);
 
   // Basis: B and D stay in shared memory for the whole kernel. The 8 x 8
@@ -186,8 +199,11 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
   const double* Gcol = A.G + static_cast<long long>(col) * nz * GSE;
   constexpr uint32_t gbytes = GSE * 8;
   const uint32_t bar = smem_u32(smem + OFF_BAR);
+  const uint32_t ubar0 = bar + 8;  // TMA path: u buffer b completes on ubar0 + 8 b
   if (tid == 0) {
     mbar_init(bar, 1);
+    if (TMA)
+      for (int b = 0; b < NUB; ++b) mbar_init(ubar0 + 8 * b, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -196,31 +212,48 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     bulk_g2s(smem_u32(Gs), Gcol + e0 * GSE, gbytes, bar, pol);
     if (e1 - e0 > 1) prefetch_l2_bulk(Gcol + (e0 + 1) * GSE, gbytes);
   }
-  // u staging of element e into buffer e % NUB: thread (i,j) of the footprint
-  // (tid < 64) copies its z-pencil into [k][j*8+i]
+  // u staging of element e into buffer (e - e0) % NUB.
+  // TMA path: one tensor copy of the 8^3 node block at (7 ex, 7 ey, 7 e),
+  // issued by one thread, completing on the buffer's mbarrier (parity
+  // ((e - e0) / NUB) & 1); readers wait on it (wait_u).
+  // cp.async path: thread (i,j) of the footprint (tid < 64) copies its z-pencil.
+  auto ubuf = [&](int e) { return Us + ((e - e0) & (NUB - 1)) * USZ; };
+  auto wait_u = [&](int e) {
+    if (TMA) mbar_wait_parity(ubar0 + 8 * ((e - e0) & (NUB - 1)), ((e - e0) / NUB) & 1);
+  };
   auto fetch_u = [&](int e) {
-    if (e < e1 && tid < N * N) {
-      const int i = tid & 7, j = tid >> 3;
-      const uint32_t dst = smem_u32(Us + (e % NUB) * US_SZ + tid);
-      const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
-      const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+    if (TMA) {
+      if (e < e1 && tid == NXW * 32) {
+        const uint32_t ub = ubar0 + 8 * ((e - e0) & (NUB - 1));
+        fence_proxy_async();  // the buffer's previous contents were read through the generic proxy
+        mbar_arrive_expect_tx(ub, USZ * 8);
+        tma_load_3d(smem_u32(ubuf(e)), &tmu, ex * P - ush, ey * P, e * P, ub);
+      }
+    } else {
+      if (e < e1 && tid < N * N) {
+        const int i = tid & 7, j = tid >> 3;
+        const uint32_t dst = smem_u32(ubuf(e) + tid);
+        const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
+        const long long plane = static_cast<long long>(A.Nx) * A.Ny;
 #pragma unroll
-      for (int k = 0; k < N; ++k) cp_async8(dst + k * US_KS * 8, A.u + base + plane * (e * P + k));
+        for (int k = 0; k < N; ++k) cp_async8(dst + k * UKS * 8, A.u + base + plane * (e * P + k));
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
   };
 
   // ------------------------------------------------ phase bodies
   // Z(e, j): z contraction of element e, pencil group j (i = g) -> SA
   auto phaseZ = [&](int e, int G) {
-    const double* us = Us + (e % NUB) * US_SZ;
+    wait_u(e);
+    const double* us = ubuf(e);
     const int X = ex * P + g, Y = ey * P + G;
     const bool bcxy = LBC && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
     double b[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int k = t + 4 * s, Z = e * P + k;
-      double v = us[k * US_KS + G * 8 + g];
+      double v = us[k * UKS + G * URS + ush + g];
       if (CON && (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi))) v = 0.0;
       b[s] = v;
     }
@@ -413,7 +446,8 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     const int Z = e * P + g, Y = ey * P + G;
     const bool zbc = CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
     // u at these nodes: still staged in shared memory (z-plane k = g of element e)
-    const double2 u2 = *reinterpret_cast<const double2*>(Us + (e % NUB) * US_SZ + g * US_KS + G * 8 + 2 * t);
+    const double* ur = ubuf(e) + g * UKS + G * URS + ush + 2 * t;
+    const double2 u2 = TMA ? make_double2(ur[0], ur[1]) : *reinterpret_cast<const double2*>(ur);
 
     // ring partials -> lateral buffer (ring.cuh layout): a ring row (j = 0 or
     // P) stores all P+1 of its nodes as one 16-byte pair per lane
@@ -466,8 +500,10 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
   // warp (c+9) % 12.
   fetch_u(e0);
   fetch_u(e0 + 1);
-  cp_async_wait<0>();
-  __syncthreads();
+  if (!TMA) {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
   if (warp < N) phaseZ(e0, warp);
   __syncthreads();
   if (warp < Q) phaseY(warp);
@@ -505,7 +541,7 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
       const int c = warp >= 9 ? warp - 9 : warp + NW - 9;
       if (c < Q) phaseY(c);
     }
-    cp_async_wait<0>();  // u(e+2), issued at the top of A_e, is read by Z(e+2) in A_{e+1}
+    if (!TMA) cp_async_wait<0>();  // u(e+2), issued at the top of A_e, is read by Z(e+2) in A_{e+1}
     __syncthreads();
   }
   double cdot = 0.0;
@@ -524,17 +560,18 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
   ring_dot_finish<NT>(A, col, cdot, s_red);
 }
 
-template <bool CON, bool DOT>
+template <bool CON, bool DOT, bool TMA>
 __global__ void __launch_bounds__(NT, 2)
-    bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs) {
+    bp3_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ MmaBasis bs,
+                      const __grid_constant__ CUtensorMap tmu) {
   if constexpr (CON) {
     const int ex = blockIdx.x % A.nx, ey = blockIdx.x / A.nx;
     if (ex > 0 && ex < A.nx - 1 && ey > 0 && ey < A.ny - 1)
-      mma_column<true, DOT, false>(A, bs);
+      mma_column<true, DOT, false, TMA>(A, bs, tmu);
     else
-      mma_column<true, DOT, true>(A, bs);
+      mma_column<true, DOT, true, TMA>(A, bs, tmu);
   } else {
-    mma_column<false, DOT, false>(A, bs);
+    mma_column<false, DOT, false, TMA>(A, bs, tmu);
   }
 }
 
@@ -543,12 +580,16 @@ __global__ void __launch_bounds__(NT, 2)
 bool mma_kernel_applies(const Setup& s) { return s.kind == KIND_DIFF && s.p == P && s.gstride == GSE; }
 
 cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static std::atomic<uint64_t> configured[4] = {};
-  const int v = (a.constrained ? 2 : 0) + (a.col_dot != nullptr ? 1 : 0);
-  const void* fns[4] = {reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, false>),
-                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, true>),
-                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, false>),
-                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, true>)};
+  static std::atomic<uint64_t> configured[8] = {};
+  const int v = (a.u_tmap ? 4 : 0) + (a.constrained ? 2 : 0) + (a.col_dot != nullptr ? 1 : 0);
+  const void* fns[8] = {reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, false, false>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, true, false>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, false, false>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, true, false>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, false, true>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<false, true, true>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, false, true>),
+                        reinterpret_cast<const void*>(&bp3_p7_mma_kernel<true, true, true>)};
   set_smem_attr_once(configured[v], fns[v], SMEM_BYTES);
   MmaBasis bs;
   for (int i = 0; i < Q; ++i)
@@ -556,23 +597,32 @@ cudaError_t launch_apply_mma(const Setup& s, const ApplyArgs& a, cudaStream_t st
       bs.B[i][j] = s.B[i * N + j];
       bs.D[i][j] = s.D[i * N + j];
     }
+  static const CUtensorMap none{};
+  const CUtensorMap& tm = a.u_tmap ? *a.u_tmap : none;
   switch (v) {
-    case 0: bp3_p7_mma_kernel<false, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
-    case 1: bp3_p7_mma_kernel<false, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
-    case 2: bp3_p7_mma_kernel<true, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
-    default: bp3_p7_mma_kernel<true, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+#define HXB_MMA_CASE(V, CON, DOT, TMA) \
+  case V: bp3_p7_mma_kernel<CON, DOT, TMA><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs, tm); break;
+    HXB_MMA_CASE(0, false, false, false)
+    HXB_MMA_CASE(1, false, true, false)
+    HXB_MMA_CASE(2, true, false, false)
+    HXB_MMA_CASE(3, true, true, false)
+    HXB_MMA_CASE(4, false, false, true)
+    HXB_MMA_CASE(5, false, true, true)
+    HXB_MMA_CASE(6, true, false, true)
+    default: bp3_p7_mma_kernel<true, true, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs, tm); break;
+#undef HXB_MMA_CASE
   }
   return cudaGetLastError();
 }
 
 void mma_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm) {
-  cudaFuncSetAttribute(&bp3_p7_mma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaFuncSetAttribute(&bp3_p7_mma_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, bp3_p7_mma_kernel<true, true>);
+  cudaFuncGetAttributes(&fa, bp3_p7_mma_kernel<true, true, false>);
   *regs = fa.numRegs;
   *smem = static_cast<int>(fa.sharedSizeBytes) + SMEM_BYTES;
   *threads = NT;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp3_p7_mma_kernel<true, true>, NT, SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp3_p7_mma_kernel<true, true, false>, NT, SMEM_BYTES);
 }
 
 }  // namespace hxb

@@ -39,20 +39,24 @@ constexpr int P = 7, N = 8;
 constexpr int NW = 8, NT = NW * 32;
 constexpr int GPL = 6 * N * N;          // one z plane of all 6 components (doubles)
 constexpr int GSE = 6 * N * N * N;      // element block of G (== Setup::gstride)
-constexpr int US_KS = 68;               // u staging [k][j*8+i], k-stride 68
-constexpr int US_SZ = N * US_KS;
+// u staging [k][j][i] (see apply_mma.cu): cp.async rows of 8, k-stride 68;
+// TMA: 10-wide boxes from the even x at or below the element, 128-byte aligned
+template <bool TMA> constexpr int us_rs() { return TMA ? N + 2 : N; }
+template <bool TMA> constexpr int us_ks() { return TMA ? N * (N + 2) : 68; }
 constexpr int NUB = 3;                  // U(e) (P), U(e+1) (Z), U(e+2) in flight
+constexpr int US_REGION = NUB * N * us_ks<true>() + 16;
+static_assert(US_REGION >= NUB * N * us_ks<false>(), "staging region");
 constexpr int TS = 9 * 64;              // [c][j][i] tiles: c-stride 72 (+ i swizzle), 8 planes
 __device__ __forceinline__ int tix(int c, int j, int i) { return c * 72 + j * 8 + (i ^ ((c & 2) << 1)); }
 constexpr int OFF_GT = 0;                     // 2 x TS
 constexpr int OFF_A3 = OFF_GT + 2 * TS;       // 2 x TS
 constexpr int OFF_W = OFF_A3 + 2 * TS;        // 2 x TS
 constexpr int OFF_U = OFF_W + 2 * TS;         // NUB x US_SZ
-constexpr int OFF_G = OFF_U + NUB * US_SZ;    // NW x GPL (16-byte aligned)
+constexpr int OFF_G = OFF_U + US_REGION;      // NW x GPL (16-byte aligned)
 constexpr int OFF_SCR = OFF_G + NW * GPL;     // NW x 64 (A2 transpose)
 constexpr int OFF_D = OFF_SCR + NW * 64;      // D (8 x 8)
-constexpr int OFF_BAR = OFF_D + 64;           // NW mbarriers
-constexpr int SMEM_BYTES = (OFF_BAR + NW) * 8;
+constexpr int OFF_BAR = OFF_D + 64;           // NW mbarriers (G planes), NUB (u buffers, TMA path)
+constexpr int SMEM_BYTES = (OFF_BAR + NW + NUB) * 8;
 static_assert(OFF_G % 2 == 0, "TMA destination must be 16-byte aligned");
 static_assert(3 * (SMEM_BYTES + 1024) <= 228 * 1024, "three CTAs per SM");
 
@@ -73,11 +77,14 @@ __device__ __forceinline__ double lds_volatile(const double* p) {
 }
 
 // CON / DOT: constrained semantics and the fused p.Ap, compile-time (see apply_mma.cu)
-template <bool CON, bool DOT>
+template <bool CON, bool DOT, bool TMA>
 __global__ void __launch_bounds__(NT, 3)
-    bp5_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ Mma5Basis bs) {
+    bp5_p7_mma_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ Mma5Basis bs,
+                      const __grid_constant__ CUtensorMap tmu) {
   extern __shared__ double smem[];
   double* Us = smem + OFF_U;
+  if (TMA) Us += ((128 - (smem_u32(Us) & 127)) & 127) / 8;  // tensor copies land 128-byte aligned
+  constexpr int UKS = us_ks<TMA>(), URS = us_rs<TMA>(), USZ = N * UKS;
   __shared__ double s_red[NW];
 
   if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
@@ -90,6 +97,7 @@ __global__ void __launch_bounds__(NT, 3)
   const int ex = col % A.nx, ey = col / A.nx;
   const int nz = A.nz;               // elements per column of the slab (G column stride)
   const int e0 = A.zr0, e1 = A.zr1;  // elements this launch marches (dist.cu overlap: sub-ranges)
+  const int ush = TMA ? (ex & 1) : 0;  // x offset of the element in a staged row (TMA box from an even x)
   const LatLayout Lat(P, A.nx, A.ny);
 
   // basis fragments (registers for the whole kernel; see apply_mma.cu)
@@ -105,29 +113,46 @@ __global__ void __launch_bounds__(NT, 3)
   double* Gp = smem + OFF_G + warp * GPL;
   const uint32_t bar = smem_u32(smem + OFF_BAR + warp);
   constexpr uint32_t pbytes = GPL * 8;
+  const uint32_t ubar0 = smem_u32(smem + OFF_BAR + NW);  // TMA path: u buffer b completes on ubar0 + 8 b
   if (lane == 0) {
     mbar_init(bar, 1);
+    if (TMA && warp == 0)
+      for (int b = 0; b < NUB; ++b) mbar_init(ubar0 + 8 * b, 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
   if (lane == 0) {
     mbar_arrive_expect_tx(bar, pbytes);
     bulk_g2s(smem_u32(Gp), Gcol + e0 * GSE + warp * GPL, pbytes, bar, pol);
   }
   if (tid == 0 && e1 - e0 > 1) prefetch_l2_bulk(Gcol + (e0 + 1) * GSE, GSE * 8);
 
-  // u staging of element e into buffer e % NUB: thread (i,j) of the footprint
-  // (tid < 64) copies its z-pencil into [k][j*8+i]
+  // u staging of element e into buffer (e - e0) % NUB: one TMA tensor copy of
+  // the 8^3 node block (TMA path, see apply_mma.cu) or thread (i,j) of the
+  // footprint (tid < 64) copying its z-pencil by cp.async
+  auto ubuf = [&](int e) { return Us + ((e - e0) % NUB) * USZ; };
+  auto wait_u = [&](int e) {
+    if (TMA) mbar_wait_parity(ubar0 + 8 * ((e - e0) % NUB), ((e - e0) / NUB) & 1);
+  };
   auto fetch_u = [&](int e) {
-    if (e < e1 && tid < N * N) {
-      const int i = tid & 7, j = tid >> 3;
-      const uint32_t dst = smem_u32(Us + (e % NUB) * US_SZ + tid);
-      const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
-      const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+    if (TMA) {
+      if (e < e1 && tid == 32) {
+        const uint32_t ub = ubar0 + 8 * ((e - e0) % NUB);
+        fence_proxy_async();  // the buffer's previous contents were read / masked through the generic proxy
+        mbar_arrive_expect_tx(ub, USZ * 8);
+        tma_load_3d(smem_u32(ubuf(e)), &tmu, ex * P - ush, ey * P, e * P, ub);
+      }
+    } else {
+      if (e < e1 && tid < N * N) {
+        const int i = tid & 7, j = tid >> 3;
+        const uint32_t dst = smem_u32(ubuf(e) + tid);
+        const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
+        const long long plane = static_cast<long long>(A.Nx) * A.Ny;
 #pragma unroll
-      for (int k = 0; k < N; ++k) cp_async8(dst + k * US_KS * 8, A.u + base + plane * (e * P + k));
+        for (int k = 0; k < N; ++k) cp_async8(dst + k * UKS * 8, A.u + base + plane * (e * P + k));
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
   };
   // ConstrainedOperator input mask P u on the staged values (each thread its
   // own copies, after cp.async completion); u^2 of the owned constrained rows
@@ -135,26 +160,28 @@ __global__ void __launch_bounds__(NT, 3)
   double dot = 0.0;
   auto mask_u = [&](int e) {
     if (e >= e1 || tid >= N * N || !CON) return;
+    wait_u(e);
     const int i = tid & 7, j = tid >> 3;
     const int X = ex * P + i, Y = ey * P + j;
     const bool bcxy = X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1;
     const bool own_xy = (i < P || ex == A.nx - 1) && (j < P || ey == A.ny - 1);
-    double* us = Us + (e % NUB) * US_SZ + tid;
+    double* us = ubuf(e) + j * URS + ush + i;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const int Z = e * P + k;
       if (bcxy || (Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)) {
         if (do_dot && own_xy && (k < P || e == nz - 1) && !(A.zlo_shared && Z == 0))
-          dot = fma(us[k * US_KS], us[k * US_KS], dot);
-        us[k * US_KS] = 0.0;
+          dot = fma(us[k * UKS], us[k * UKS], dot);
+        us[k * UKS] = 0.0;
       }
     }
   };
 
   // ------------------------------------------------ phase bodies
   auto phaseZ = [&](int e, int G) {  // gt = D_z u, j group G -> GT
-    const double* us = Us + (e % NUB) * US_SZ;
-    const double b0 = us[t * US_KS + G * 8 + g], b1 = us[(t + 4) * US_KS + G * 8 + g];
+    wait_u(e);
+    const double* us = ubuf(e);
+    const double b0 = us[t * UKS + G * URS + ush + g], b1 = us[(t + 4) * UKS + G * URS + ush + g];
     double c0 = 0.0, c1 = 0.0;
     dmma(c0, c1, aD0, b0);
     dmma(c0, c1, aD1, b1);
@@ -162,10 +189,10 @@ __global__ void __launch_bounds__(NT, 3)
   };
 
   auto phaseP = [&](int e, int c) {  // z plane c of element e
-    const double* us = Us + (e % NUB) * US_SZ + c * US_KS;
+    const double* us = ubuf(e) + c * UKS + ush;
     // gr (transposed form, rows j = g, cols a = 2t, 2t+1); gs (standard form, same layout)
-    const double ua0 = us[g * 8 + t], ua1 = us[g * 8 + t + 4];
-    const double ub0 = us[t * 8 + g], ub1 = us[(t + 4) * 8 + g];
+    const double ua0 = us[g * URS + t], ua1 = us[g * URS + t + 4];
+    const double ub0 = us[t * URS + g], ub1 = us[(t + 4) * URS + g];
     double gr[2] = {0.0, 0.0}, gs[2] = {0.0, 0.0};
     dmma(gr[0], gr[1], ua0, aD0);
     dmma(gr[0], gr[1], ua1, aD1);
@@ -251,7 +278,9 @@ __global__ void __launch_bounds__(NT, 3)
         A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
       } else {
         const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-        A.w[node] = zbc ? __ldg(A.u + node) : o[q];  // ConstrainedOperator rows: w = u
+        const long long unode =  // u may be row-pitched (ApplyArgs::u_pitch)
+            TMA ? X + static_cast<long long>(A.u_pitch) * (Y + static_cast<long long>(A.Ny) * Z) : node;
+        A.w[node] = zbc ? __ldg(A.u + unode) : o[q];  // ConstrainedOperator rows: w = u
       }
     }
   };
@@ -259,7 +288,7 @@ __global__ void __launch_bounds__(NT, 3)
   // ------------------------------------------------ schedule: A_e = P(e) || Z(e+1) || Z'(e-1)
   fetch_u(e0);
   fetch_u(e0 + 1);
-  cp_async_wait<0>();
+  if (!TMA) cp_async_wait<0>();
   mask_u(e0);
   mask_u(e0 + 1);
   __syncthreads();
@@ -272,7 +301,7 @@ __global__ void __launch_bounds__(NT, 3)
     if (e > e0) phaseZp(e - 1, warp);
     if (e + 1 < e1) phaseZ(e + 1, warp);
     if (e == e1) break;
-    cp_async_wait<0>();
+    if (!TMA) cp_async_wait<0>();
     mask_u(e + 2);
     __syncthreads();
   }
@@ -298,33 +327,46 @@ bool mma5_kernel_applies(const Setup& s) { return s.kind == KIND_COLLOC && s.p =
 
 cudaError_t launch_apply_mma5(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   if (s.gstride != GSE) return cudaErrorInvalidValue;
-  static std::atomic<uint64_t> configured[4] = {};
-  const int v = (a.constrained ? 2 : 0) + (a.col_dot != nullptr ? 1 : 0);
-  const void* fns[4] = {reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, false>),
-                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, true>),
-                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, false>),
-                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, true>)};
+  static std::atomic<uint64_t> configured[8] = {};
+  const int v = (a.u_tmap ? 4 : 0) + (a.constrained ? 2 : 0) + (a.col_dot != nullptr ? 1 : 0);
+  const void* fns[8] = {reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, false, false>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, true, false>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, false, false>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, true, false>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, false, true>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<false, true, true>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, false, true>),
+                        reinterpret_cast<const void*>(&bp5_p7_mma_kernel<true, true, true>)};
   set_smem_attr_once(configured[v], fns[v], SMEM_BYTES);
   Mma5Basis bs;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) bs.D[i][j] = s.D[i * N + j];
+  static const CUtensorMap none{};
+  const CUtensorMap& tm = a.u_tmap ? *a.u_tmap : none;
   switch (v) {
-    case 0: bp5_p7_mma_kernel<false, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
-    case 1: bp5_p7_mma_kernel<false, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
-    case 2: bp5_p7_mma_kernel<true, false><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
-    default: bp5_p7_mma_kernel<true, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs); break;
+#define HXB_MMA5_CASE(V, CON, DOT, TMA) \
+  case V: bp5_p7_mma_kernel<CON, DOT, TMA><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs, tm); break;
+    HXB_MMA5_CASE(0, false, false, false)
+    HXB_MMA5_CASE(1, false, true, false)
+    HXB_MMA5_CASE(2, true, false, false)
+    HXB_MMA5_CASE(3, true, true, false)
+    HXB_MMA5_CASE(4, false, false, true)
+    HXB_MMA5_CASE(5, false, true, true)
+    HXB_MMA5_CASE(6, true, false, true)
+    default: bp5_p7_mma_kernel<true, true, true><<<a.ncols, NT, SMEM_BYTES, st>>>(a, bs, tm); break;
+#undef HXB_MMA5_CASE
   }
   return cudaGetLastError();
 }
 
 void mma5_kernel_info(int* regs, int* smem, int* threads, int* blocks_per_sm) {
-  cudaFuncSetAttribute(&bp5_p7_mma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaFuncSetAttribute(&bp5_p7_mma_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, bp5_p7_mma_kernel<true, true>);
+  cudaFuncGetAttributes(&fa, bp5_p7_mma_kernel<true, true, false>);
   *regs = fa.numRegs;
   *smem = static_cast<int>(fa.sharedSizeBytes) + SMEM_BYTES;
   *threads = NT;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp5_p7_mma_kernel<true, true>, NT, SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, bp5_p7_mma_kernel<true, true, false>, NT, SMEM_BYTES);
 }
 
 }  // namespace hxb

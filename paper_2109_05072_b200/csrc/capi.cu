@@ -445,6 +445,13 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
   al(reinterpret_cast<void**>(&w.dot_result), sizeof(double) * 2);
   al(reinterpret_cast<void**>(&w.vec_done), sizeof(unsigned int) * 4);
   al(reinterpret_cast<void**>(&w.history), sizeof(double) * w.history_cap);
+  if (!e && tma_u_supported(s)) {  // row-pitched search direction of the fast CG (tma.cu)
+    w.pt_pitch = tma_u_pitch(s);
+    al(reinterpret_cast<void**>(&w.pt), sizeof(double) * static_cast<std::size_t>(w.pt_pitch) *
+                                            (static_cast<std::size_t>(s.dims[1]) * s.p + 1) *
+                                            (static_cast<std::size_t>(s.dims[2]) * s.p + 1));
+    if (!e) e = encode_u_tensor_map(s, w.pt, w.pt_pitch, &w.pt_map);
+  }
   if (!e) e = cudaMallocHost(reinterpret_cast<void**>(&w.host_sc), sizeof(DevScalars));
   if (e) {
     hexbp_workspace_destroy(wh);
@@ -469,7 +476,7 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
   void* bufs[] = {w.mp_buf, w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.tmp_d, w.vec_partials,
-                  w.vec_done, w.history, w.dot_result};
+                  w.vec_done, w.history, w.dot_result, w.pt};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (w.host_sc) cudaFreeHost(w.host_sc);
@@ -485,6 +492,27 @@ int hexbp_apply(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* 
   if (u == w) return invalid("apply: u and w must not alias");
   DeviceGuard g(h->s.device);
   CK(launch_apply(h->s, wh->w, u, w, constrained, nullptr, nullptr, static_cast<cudaStream_t>(stream)));
+  return HEXBP_OK;
+}
+
+int hexbp_apply_cg_form(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, double* w, int constrained,
+                        void* stream) {
+  if (!h || !wh || !w) return invalid("apply_cg_form: null argument");
+  if (wh->w.s != &h->s) return invalid("apply: workspace belongs to another setup");
+  Workspace& ws = wh->w;
+  if (ws.exact && !ws.fast_op) return invalid("apply_cg_form: fast-mode workspaces only");
+  const Setup& s = h->s;
+  DeviceGuard g(s.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* pv = ws.pt && !ws.exact ? ws.pt : ws.p;
+  if (u == w || pv == w) return invalid("apply_cg_form: u / the search direction and w must not alias");
+  if (u) {
+    const size_t Nx = static_cast<size_t>(s.dims[0]) * s.p + 1;
+    const size_t rows = static_cast<size_t>(s.nL) / Nx;
+    const size_t pitch = pv == ws.pt ? static_cast<size_t>(ws.pt_pitch) : Nx;
+    CK(cudaMemcpy2DAsync(pv, pitch * 8, u, Nx * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(launch_apply(s, ws, pv, w, constrained, nullptr, nullptr, st, false));
   return HEXBP_OK;
 }
 
@@ -595,6 +623,14 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
       cudaMemsetAsync(reinterpret_cast<char*>(w.sc) + offsetof(DevScalars, precond), 0, sizeof(int), st);
     }
   } clear_diag{w, st};
+  // fast CG on the DMMA degrees: the search direction lives row-pitched in
+  // Workspace::pt so the operator stages it by TMA tensor copies (tma.cu)
+  struct UsePt {
+    Workspace& w;
+    ~UsePt() { w.use_pt = 0; }
+  } use_pt{w};
+  w.use_pt = !w.exact && w.pt != nullptr;
+  double* const pv = w.use_pt ? w.pt : w.p;
   // r0 = b - A x0 (solver.hpp:102-103); fast mode sums the ring in the init kernel
   if (w.exact) {
     CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
@@ -612,7 +648,7 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
       CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, st));
       CK(launch_cg_pap(w, n, st));
     } else {
-      CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
+      CK(launch_apply(s, w, pv, w.Ap, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
     }
     CK(launch_cg_update_r(w, n, st, constrained));
     if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz_next = r.z, beta (solver.hpp:145-147)

@@ -308,6 +308,75 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
   }
 }
 
+// The same fast-mode update with p row-pitched (Workspace::pt): node i of
+// x / r / diag is node (X, row) = divmod(i, Nx) of p, at row * pitch + X.
+// Grid-stride like cg_update_xp_kernel (four independent streams per thread),
+// with each stream's (row, X) advanced by a precomputed divmod of the step
+// instead of a division per node.
+struct StepDivmod {
+  int q4, r4;  // divmod(4 * stride, Nx)
+  int q1, r1;  // divmod(stride, Nx)
+};
+template <bool PC>
+__global__ void __launch_bounds__(VT) cg_update_xp_pitched_kernel(double* __restrict__ x, double* __restrict__ p,
+                                                                  const double* __restrict__ r, long long n, int Nx,
+                                                                  int pitch, StepDivmod sd, unsigned int* done,
+                                                                  DevScalars* sc, const double* __restrict__ dv) {
+  if (*(volatile int*)&sc->x_pending == 0) return;
+  const double alpha = sc->alpha, beta = sc->beta;
+  const bool update_p = *(volatile int*)&sc->status == ST_RUNNING;
+  const long long stride = static_cast<long long>(gridDim.x) * VT;
+  long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x;
+  const long long pad = pitch - Nx;
+  long long row[4];
+  int X[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const long long iu = i + u * stride;
+    row[u] = iu / Nx;
+    X[u] = static_cast<int>(iu - row[u] * Nx);
+  }
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    double pv[4], xv[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pv[u] = p[i + u * stride + row[u] * pad];
+      xv[u] = x[i + u * stride];
+      rv[u] = update_p ? r[i + u * stride] : 0.0;
+      if (PC && update_p) rv[u] = rv[u] / dv[i + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[i + u * stride] = fma(alpha, pv[u], xv[u]);
+      if (update_p) p[i + u * stride + row[u] * pad] = fma(beta, pv[u], rv[u]);
+      X[u] += sd.r4;
+      row[u] += sd.q4;
+      if (X[u] >= Nx) {
+        X[u] -= Nx;
+        ++row[u];
+      }
+    }
+  }
+  for (; i < n; i += stride) {
+    const long long pi = i + row[0] * pad;
+    const double pvi = p[pi];
+    const double zi = update_p ? (PC ? r[i] / dv[i] : r[i]) : 0.0;
+    x[i] = fma(alpha, pvi, x[i]);
+    if (update_p) p[pi] = fma(beta, pvi, zi);
+    X[0] += sd.r1;
+    row[0] += sd.q1;
+    if (X[0] >= Nx) {
+      X[0] -= Nx;
+      ++row[0];
+    }
+  }
+  if (!last_block(done)) return;
+  if (threadIdx.x == 0) {
+    sc->x_pending = 0;
+    *done = 0;
+  }
+}
+
 // ---- FUSED mode: FMA updates and fixed-order tree reductions.
 __device__ __forceinline__ double tree_partials(const double* part, int nblk, double* red) {
   double s = 0.0;
@@ -380,6 +449,7 @@ struct RingUpdateArgs {
   // block stores this rank's r.r there instead of running the scalar step.
   int zlo_asm, zhi_asm;
   double* rank_partial;
+  int p_pitch, pout_pitch;  // row pitches of p and pout (Workspace::pt: Nx rounded up to even)
 };
 
 // INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
@@ -407,10 +477,10 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
     const bool bcrow = R.constrained && (Y == 0 || Y == R.Ny - 1 || (Z == 0 && R.bc_zlo) || (Z == R.Nz - 1 && R.bc_zhi));
     double* rr_ = R.r + static_cast<long long>(R.Nx) * row;
     const double* ap = R.Ap + static_cast<long long>(R.Nx) * row;
-    const double* pp = R.p + static_cast<long long>(R.Nx) * row;
+    const double* pp = R.p + static_cast<long long>(R.p_pitch) * row;
     const double* dd = PC ? R.dv + static_cast<long long>(R.Nx) * row : nullptr;
     const double* bb = INIT ? R.b + static_cast<long long>(R.Nx) * row : nullptr;
-    double* po = INIT ? R.pout + static_cast<long long>(R.Nx) * row : nullptr;
+    double* po = INIT ? R.pout + static_cast<long long>(R.pout_pitch) * row : nullptr;
     if ((Z == 0 && R.zlo_asm) || (Z == R.Nz - 1 && R.zhi_asm)) {
       // shared node plane, already assembled in Ap (constrained nodes: A p = p)
       const bool owned = !(Z == 0 && R.zlo_asm);
@@ -770,11 +840,14 @@ cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int c
   RingUpdateArgs R;
   R.Ap = ws.Ap;
   R.p = p_applied;
+  const int Nx = s.dims[0] * s.p + 1;
+  R.p_pitch = ws.pt != nullptr && p_applied == ws.pt ? ws.pt_pitch : Nx;
   R.latY = ws.lateral;
   R.latX = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
   R.dv = ws.diag;
   R.b = b;
-  R.pout = ws.p;
+  R.pout = ws.use_pt ? ws.pt : ws.p;
+  R.pout_pitch = ws.use_pt ? ws.pt_pitch : Nx;
   R.rel_tol = rel_tol;
   R.max_iter = max_iter;
   R.r = ws.r;
@@ -821,7 +894,7 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
     return cudaGetLastError();
   }
   // fast mode: A p comes from launch_apply(..., finish_ring = false)
-  return launch_ring_r<false>(ws, n, st, constrained, ws.p, nullptr, 0.0, 0);
+  return launch_ring_r<false>(ws, n, st, constrained, ws.use_pt ? ws.pt : ws.p, nullptr, 0.0, 0);
 }
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
@@ -843,8 +916,19 @@ cudaError_t launch_cg_init_ring(const Workspace& ws, const double* b, const doub
 }
 
 cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaStream_t st, double* p) {
-  if (!p) p = ws.p;
+  if (!p) p = ws.use_pt ? ws.pt : ws.p;
   const int g = vec_grid(n);
+  const int Nx = ws.s->dims[0] * ws.s->p + 1;
+  if (ws.pt != nullptr && p == ws.pt && !ws.exact) {  // row-pitched search direction (tma.cu)
+    const long long stride = static_cast<long long>(g) * VT;
+    const StepDivmod sd{static_cast<int>(4 * stride / Nx), static_cast<int>(4 * stride % Nx),
+                        static_cast<int>(stride / Nx), static_cast<int>(stride % Nx)};
+    if (ws.diag)
+      cg_update_xp_pitched_kernel<true><<<g, VT, 0, st>>>(x, p, ws.r, n, Nx, ws.pt_pitch, sd, ws.vec_done, ws.sc, ws.diag);
+    else
+      cg_update_xp_pitched_kernel<false><<<g, VT, 0, st>>>(x, p, ws.r, n, Nx, ws.pt_pitch, sd, ws.vec_done, ws.sc, nullptr);
+    return cudaGetLastError();
+  }
   if (ws.exact) {
     if (ws.diag)
       cg_update_xp_kernel<true, true><<<g, VT, 0, st>>>(x, p, ws.r, n, ws.vec_done, ws.sc, ws.diag);

@@ -2,6 +2,7 @@
 // Public C ABI: include/hexbp_b200.h.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -83,6 +84,12 @@ struct ApplyArgs {
   // launch_carry_combine -- the multi-GPU overlap of dist.cu.
   double* carry_lo;
   double* carry_hi;
+  // Row-pitched input (the single-GPU fast CG's search direction, Workspace::pt):
+  // node (X, Y, Z) of u at X + u_pitch (Y + Ny Z). u_pitch = 0: unpadded (Nx).
+  // With u_tmap (host pointer, read by the launcher) the DMMA kernels stage
+  // each element's 8^3 node block by one TMA tensor copy.
+  int u_pitch;
+  const CUtensorMap* u_tmap;
 };
 
 struct Setup {
@@ -120,6 +127,13 @@ struct Workspace {
   double* r = nullptr;
   double* p = nullptr;
   double* Ap = nullptr;
+  // Row-pitched copy of the search direction for the single-GPU fast CG on
+  // the DMMA degrees (row pitch Nx rounded up to even: 16-byte row strides,
+  // as a TMA tensor map requires), and its 3D tensor map (box = one element).
+  double* pt = nullptr;
+  int pt_pitch = 0;
+  CUtensorMap pt_map;
+  int use_pt = 0;  // set by the fast CG for the duration of a solve (capi.cu pcg_run)
   double* tmp_u = nullptr;  // host-API staging
   double* tmp_w = nullptr;
   double* tmp_d = nullptr;  // host-API Jacobi diagonal staging
@@ -142,6 +156,11 @@ struct Workspace {
 };
 
 // ---- apply.cu
+// Setups whose fast operator kernel stages u by TMA tensor copies from a
+// row-pitched vector (the DMMA kernels); tma.cu encodes the maps.
+bool tma_u_supported(const Setup& s);
+int tma_u_pitch(const Setup& s);
+cudaError_t encode_u_tensor_map(const Setup& s, const double* u, int pitch, CUtensorMap* map);
 // finish_ring = false leaves the ring nodes of w as lateral partials (CG fast
 // mode: launch_cg_update_r sums them).
 ApplyArgs make_apply_args(const Setup& s, const Workspace& ws, const double* u, double* w, int constrained,

@@ -27,7 +27,7 @@ ks = sorted([(ev.time_range.start, ev.time_range.end, ev.name) for ev in evs], k
 agg = {}
 gaps = []
 for i, (s, t, n) in enumerate(ks):
-    k = n.split("(")[0][-40:]
+    k = n.replace("(anonymous namespace)::", "").split("(")[0][-60:]
     agg.setdefault(k, []).append(t - s)
     if i:
         gaps.append((s - ks[i - 1][1], ks[i - 1][2].split("(")[0][-30:] + f" #{i - 1}", k + f" #{i}"))

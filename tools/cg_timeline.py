@@ -11,10 +11,11 @@ from torch.profiler import ProfilerActivity, profile
 import paper_2109_05072_b200 as hx
 
 e = int(os.environ.get("E", "66"))
+bp, p = int(os.environ.get("BP", "3")), int(os.environ.get("P", "7"))
 dims = (e, e, e)
-op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind.BP3, hx.build_box_mesh(dims, 7)))
-A = hx.ConstrainedOperator(op)
-b = torch.from_numpy(hx.bench_rhs(3, 7, dims)).cuda()
+op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), hx.build_box_mesh(dims, p)))
+A = hx.ConstrainedOperator(op) if bp != 1 else op
+b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda()
 x = torch.zeros_like(b)
 hx.cg(A, b, x, 0.0, 5, mode="fast")
 x.zero_()

@@ -450,7 +450,13 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
     al(reinterpret_cast<void**>(&w.pt), sizeof(double) * static_cast<std::size_t>(w.pt_pitch) *
                                             (static_cast<std::size_t>(s.dims[1]) * s.p + 1) *
                                             (static_cast<std::size_t>(s.dims[2]) * s.p + 1));
-    if (!e) e = encode_u_tensor_map(s, w.pt, w.pt_pitch, &w.pt_map);
+    // no tensor map (driver without cuTensorMapEncodeTiled): the fast CG keeps
+    // the unpadded p and the cp.async-staged kernels
+    if (!e && encode_u_tensor_map(s, w.pt, w.pt_pitch, &w.pt_map) != cudaSuccess) {
+      cudaFree(w.pt);
+      w.pt = nullptr;
+      w.pt_pitch = 0;
+    }
   }
   if (!e) e = cudaMallocHost(reinterpret_cast<void**>(&w.host_sc), sizeof(DevScalars));
   if (e) {

@@ -455,13 +455,16 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     if (rowring)
       *reinterpret_cast<double2*>(A.lateral + Lat.y_index(P, A.nx, Z, ey + (G == P), G == 0, ex, 2 * t)) =
           make_double2(o[0], o[1]);
+#ifdef HX_NO_HOLEFILL
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const double uv = q ? u2.y : u2.x;
       const int i = 2 * t + q, X = ex * P + i;
       const bool ring = rowring || i == 0 || i == P;
       if (ring) {
-        if (!rowring) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
+        if (!rowring) {
+          A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
+        }
         if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
           if (zbc || (LBC && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
             if (ring_owner(P, i, G, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0))
@@ -479,6 +482,50 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     }
   };
 
+#else
+    if (!rowring) {
+      // The row's P+1 nodes go to w, the two x-face nodes (i = 0, P) with
+      // this column's partial: their w value is never read (the r-update /
+      // lateral fix-up supplies them from latX; the neighbour column's store
+      // of its own partial may win), but complete rows turn the L2's
+      // evictions of this row's 32-byte sectors into full-sector writes
+      // instead of DRAM read-modify-writes of ECC sectors (-0.38 GB of DRAM
+      // reads per apply at cfg3), and the lanes' node pairs are 16-byte
+      // stores whenever the row starts at an even node (parity uniform per row).
+      const long long node0 =
+          ex * P + 2 * t + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+      const double v0 = (zbc && t != 0) ? u2.x : o[0];      // i = 2t     (x-face at t = 0)
+      const double v1 = (zbc && t != 3) ? u2.y : o[1];      // i = 2t + 1 (x-face at t = 3)
+      if ((node0 & 1) == 0) {
+        *reinterpret_cast<double2*>(A.w + node0) = make_double2(v0, v1);
+      } else {
+        A.w[node0] = v0;
+        A.w[node0 + 1] = v1;
+      }
+      if (t == 0) A.lat_x[Lat.x_index(A.nx, Z, Y, ex, 1)] = o[0];
+      if (t == 3) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + 1, 0)] = o[1];
+    }
+    if (do_dot) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double uv = q ? u2.y : u2.x;
+        const int i = 2 * t + q, X = ex * P + i;
+        const bool ring = rowring || i == 0 || i == P;
+        if (ring) {  // column-local share of p.Ap on the ring (ring.cuh)
+          if (zbc || (LBC && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
+            if (ring_owner(P, i, G, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0))
+              dot = fma(uv, uv, dot);  // w = u, counted once
+          } else {
+            dot = fma(uv, o[q], dot);
+          }
+        } else {
+          dot = fma(uv, zbc ? uv : o[q], dot);
+        }
+      }
+    }
+  };
+
+#endif
   auto phaseZp = [&](int e, int G) {
     double o[2];
     phaseZpMath(G, o);

@@ -271,18 +271,25 @@ __global__ void __launch_bounds__(NT, 3)
           make_double2(o[0], o[1]);
       return;
     }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int i = 2 * t + q, X = ex * P + i;
-      if (i == 0 || i == P) {
-        A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
-      } else {
-        const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-        const long long unode =  // u may be row-pitched (ApplyArgs::u_pitch)
-            TMA ? X + static_cast<long long>(A.u_pitch) * (Y + static_cast<long long>(A.Ny) * Z) : node;
-        A.w[node] = zbc ? __ldg(A.u + unode) : o[q];  // ConstrainedOperator rows: w = u
-      }
+    // the row's P+1 nodes go to w, the x-face nodes (i = 0, P) with this
+    // column's partial (never read; full-sector L2 evictions instead of DRAM
+    // read-modify-writes, see apply_mma.cu), and their partials to latX
+    const long long node0 = ex * P + 2 * t + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+    double v[2] = {o[0], o[1]};
+    if (zbc) {  // ConstrainedOperator rows: w = u (u may be row-pitched, ApplyArgs::u_pitch)
+      const long long unode0 =
+          TMA ? ex * P + 2 * t + static_cast<long long>(A.u_pitch) * (Y + static_cast<long long>(A.Ny) * Z) : node0;
+      if (t != 0) v[0] = __ldg(A.u + unode0);
+      if (t != 3) v[1] = __ldg(A.u + unode0 + 1);
     }
+    if ((node0 & 1) == 0) {  // parity uniform per row
+      *reinterpret_cast<double2*>(A.w + node0) = make_double2(v[0], v[1]);
+    } else {
+      A.w[node0] = v[0];
+      A.w[node0 + 1] = v[1];
+    }
+    if (t == 0) A.lat_x[Lat.x_index(A.nx, Z, Y, ex, 1)] = o[0];
+    if (t == 3) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + 1, 0)] = o[1];
   };
 
   // ------------------------------------------------ schedule: A_e = P(e) || Z(e+1) || Z'(e-1)

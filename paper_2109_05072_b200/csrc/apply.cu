@@ -1293,8 +1293,9 @@ ApplyArgs make_apply_args(const Setup& s, const Workspace& ws, const double* u, 
   a.zr1 = s.dims[2];
   if (ws.pt != nullptr && u == ws.pt) {  // the fast CG's row-pitched search direction (tma.cu)
     a.u_pitch = ws.pt_pitch;
-    a.u_tmap = &ws.pt_map;
+    a.u_tmap = tma_u_staging_enabled() ? &ws.pt_map : nullptr;
   }
+  if (ws.Apt != nullptr && w == ws.Apt) a.w_pitch = ws.pt_pitch;  // its row-pitched A p
   return a;
 }
 

@@ -233,8 +233,9 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
       if (e < e1 && tid < N * N) {
         const int i = tid & 7, j = tid >> 3;
         const uint32_t dst = smem_u32(ubuf(e) + tid);
-        const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
-        const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+        const long long upitch = A.u_pitch ? A.u_pitch : A.Nx;  // u may be row-pitched
+        const long long base = (ex * P + i) + upitch * (ey * P + j);
+        const long long plane = upitch * A.Ny;
 #pragma unroll
         for (int k = 0; k < N; ++k) cp_async8(dst + k * UKS * 8, A.u + base + plane * (e * P + k));
       }
@@ -455,34 +456,6 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     if (rowring)
       *reinterpret_cast<double2*>(A.lateral + Lat.y_index(P, A.nx, Z, ey + (G == P), G == 0, ex, 2 * t)) =
           make_double2(o[0], o[1]);
-#ifdef HX_NO_HOLEFILL
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double uv = q ? u2.y : u2.x;
-      const int i = 2 * t + q, X = ex * P + i;
-      const bool ring = rowring || i == 0 || i == P;
-      if (ring) {
-        if (!rowring) {
-          A.lat_x[Lat.x_index(A.nx, Z, Y, ex + (i == P), i == 0)] = o[q];
-        }
-        if (do_dot) {  // column-local share of p.Ap on the ring (ring.cuh)
-          if (zbc || (LBC && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1))) {
-            if (ring_owner(P, i, G, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0))
-              dot = fma(uv, uv, dot);  // w = u, counted once
-          } else {
-            dot = fma(uv, o[q], dot);
-          }
-        }
-      } else {
-        const long long node = X + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
-        const double v = zbc ? uv : o[q];
-        A.w[node] = v;
-        if (do_dot) dot = fma(uv, v, dot);
-      }
-    }
-  };
-
-#else
     if (!rowring) {
       // The row's P+1 nodes go to w, the two x-face nodes (i = 0, P) with
       // this column's partial: their w value is never read (the r-update /
@@ -492,8 +465,8 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
       // instead of DRAM read-modify-writes of ECC sectors (-0.38 GB of DRAM
       // reads per apply at cfg3), and the lanes' node pairs are 16-byte
       // stores whenever the row starts at an even node (parity uniform per row).
-      const long long node0 =
-          ex * P + 2 * t + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+      const long long node0 =  // w may be row-pitched (ApplyArgs::w_pitch)
+          ex * P + 2 * t + static_cast<long long>(A.w_pitch ? A.w_pitch : A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
       const double v0 = (zbc && t != 0) ? u2.x : o[0];      // i = 2t     (x-face at t = 0)
       const double v1 = (zbc && t != 3) ? u2.y : o[1];      // i = 2t + 1 (x-face at t = 3)
       if ((node0 & 1) == 0) {
@@ -525,7 +498,6 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     }
   };
 
-#endif
   auto phaseZp = [&](int e, int G) {
     double o[2];
     phaseZpMath(G, o);

@@ -146,8 +146,9 @@ __global__ void __launch_bounds__(NT, 3)
       if (e < e1 && tid < N * N) {
         const int i = tid & 7, j = tid >> 3;
         const uint32_t dst = smem_u32(ubuf(e) + tid);
-        const long long base = (ex * P + i) + static_cast<long long>(A.Nx) * (ey * P + j);
-        const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+        const long long upitch = A.u_pitch ? A.u_pitch : A.Nx;  // u may be row-pitched
+        const long long base = (ex * P + i) + upitch * (ey * P + j);
+        const long long plane = upitch * A.Ny;
 #pragma unroll
         for (int k = 0; k < N; ++k) cp_async8(dst + k * UKS * 8, A.u + base + plane * (e * P + k));
       }
@@ -274,11 +275,12 @@ __global__ void __launch_bounds__(NT, 3)
     // the row's P+1 nodes go to w, the x-face nodes (i = 0, P) with this
     // column's partial (never read; full-sector L2 evictions instead of DRAM
     // read-modify-writes, see apply_mma.cu), and their partials to latX
-    const long long node0 = ex * P + 2 * t + static_cast<long long>(A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
+    const long long node0 =  // w may be row-pitched (ApplyArgs::w_pitch)
+        ex * P + 2 * t + static_cast<long long>(A.w_pitch ? A.w_pitch : A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
     double v[2] = {o[0], o[1]};
     if (zbc) {  // ConstrainedOperator rows: w = u (u may be row-pitched, ApplyArgs::u_pitch)
       const long long unode0 =
-          TMA ? ex * P + 2 * t + static_cast<long long>(A.u_pitch) * (Y + static_cast<long long>(A.Ny) * Z) : node0;
+          ex * P + 2 * t + static_cast<long long>(A.u_pitch ? A.u_pitch : A.Nx) * (Y + static_cast<long long>(A.Ny) * Z);
       if (t != 0) v[0] = __ldg(A.u + unode0);
       if (t != 3) v[1] = __ldg(A.u + unode0 + 1);
     }

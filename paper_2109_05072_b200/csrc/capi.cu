@@ -445,16 +445,21 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
   al(reinterpret_cast<void**>(&w.dot_result), sizeof(double) * 2);
   al(reinterpret_cast<void**>(&w.vec_done), sizeof(unsigned int) * 4);
   al(reinterpret_cast<void**>(&w.history), sizeof(double) * w.history_cap);
-  if (!e && tma_u_supported(s)) {  // row-pitched search direction of the fast CG (tma.cu)
+  if (!e && tma_u_supported(s)) {  // row-pitched vectors of the fast CG (tma.cu)
     w.pt_pitch = tma_u_pitch(s);
-    al(reinterpret_cast<void**>(&w.pt), sizeof(double) * static_cast<std::size_t>(w.pt_pitch) *
-                                            (static_cast<std::size_t>(s.dims[1]) * s.p + 1) *
-                                            (static_cast<std::size_t>(s.dims[2]) * s.p + 1));
+    const std::size_t np = sizeof(double) * static_cast<std::size_t>(w.pt_pitch) *
+                           (static_cast<std::size_t>(s.dims[1]) * s.p + 1) * (static_cast<std::size_t>(s.dims[2]) * s.p + 1);
+    al(reinterpret_cast<void**>(&w.pt), np);
+    al(reinterpret_cast<void**>(&w.xt), np);
+    al(reinterpret_cast<void**>(&w.rt), np);
+    al(reinterpret_cast<void**>(&w.Apt), np);
     // no tensor map (driver without cuTensorMapEncodeTiled): the fast CG keeps
     // the unpadded p and the cp.async-staged kernels
     if (!e && encode_u_tensor_map(s, w.pt, w.pt_pitch, &w.pt_map) != cudaSuccess) {
-      cudaFree(w.pt);
-      w.pt = nullptr;
+      for (double** b : {&w.pt, &w.xt, &w.rt, &w.Apt}) {
+        cudaFree(*b);
+        *b = nullptr;
+      }
       w.pt_pitch = 0;
     }
   }
@@ -482,7 +487,7 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
   Workspace& w = wh->w;
   DeviceGuard g(w.device);
   void* bufs[] = {w.mp_buf, w.lateral, w.zupper, w.fix_partials, w.fix_done,  w.col_dot, w.sc, w.r, w.p, w.Ap, w.tmp_u, w.tmp_w, w.tmp_d, w.vec_partials,
-                  w.vec_done, w.history, w.dot_result, w.pt};
+                  w.vec_done, w.history, w.dot_result, w.pt, w.xt, w.rt, w.Apt};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (w.host_sc) cudaFreeHost(w.host_sc);
@@ -629,21 +634,29 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
       cudaMemsetAsync(reinterpret_cast<char*>(w.sc) + offsetof(DevScalars, precond), 0, sizeof(int), st);
     }
   } clear_diag{w, st};
-  // fast CG on the DMMA degrees: the search direction lives row-pitched in
-  // Workspace::pt so the operator stages it by TMA tensor copies (tma.cu)
+  // fast CG on the DMMA degrees (unpreconditioned): the search direction
+  // lives row-pitched in Workspace::pt so the operator stages it by TMA
+  // tensor copies (tma.cu), and x, r, A p share that pitch (xt, rt, Apt) so
+  // the vector kernels stay 32-byte aligned across operands; x is copied in
+  // here and out after the loop
   struct UsePt {
     Workspace& w;
     ~UsePt() { w.use_pt = 0; }
   } use_pt{w};
-  w.use_pt = !w.exact && w.pt != nullptr;
+  w.use_pt = !w.exact && w.pt != nullptr && diag == nullptr;
   double* const pv = w.use_pt ? w.pt : w.p;
+  double* const xv = w.use_pt ? w.xt : x;
+  double* const apv = w.use_pt ? w.Apt : w.Ap;
+  const size_t Nx = static_cast<size_t>(s.dims[0]) * s.p + 1, rows = static_cast<size_t>(n) / Nx;
+  if (w.use_pt)
+    CK(cudaMemcpy2DAsync(w.xt, w.pt_pitch * 8, x, Nx * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
   // r0 = b - A x0 (solver.hpp:102-103); fast mode sums the ring in the init kernel
   if (w.exact) {
     CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
     if (b_ready) CK(cudaStreamWaitEvent(st, b_ready, 0));
     CK(launch_cg_init(w, b, n, rel_tol, max_iter, st));
   } else {
-    CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st, /*finish_ring=*/false));
+    CK(launch_apply(s, w, x, apv, constrained, nullptr, nullptr, st, /*finish_ring=*/false));
     if (b_ready) CK(cudaStreamWaitEvent(st, b_ready, 0));
     CK(launch_cg_init_ring(w, b, x, n, rel_tol, max_iter, constrained, st));
   }
@@ -654,17 +667,19 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
       CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, st));
       CK(launch_cg_pap(w, n, st));
     } else {
-      CK(launch_apply(s, w, pv, w.Ap, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
+      CK(launch_apply(s, w, pv, apv, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
     }
     CK(launch_cg_update_r(w, n, st, constrained));
     if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz_next = r.z, beta (solver.hpp:145-147)
-    CK(launch_cg_update_xp(w, x, n, st));
+    CK(launch_cg_update_xp(w, xv, n, st));
     if (k % check_every == 0 && k < max_iter) {
       CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       if (w.host_sc->status != ST_RUNNING) break;
     }
   }
+  if (w.use_pt)
+    CK(cudaMemcpy2DAsync(x, Nx * 8, w.xt, w.pt_pitch * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const DevScalars hs = *w.host_sc;

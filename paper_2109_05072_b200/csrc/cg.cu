@@ -308,75 +308,6 @@ __global__ void __launch_bounds__(VT) cg_update_xp_kernel(double* __restrict__ x
   }
 }
 
-// The same fast-mode update with p row-pitched (Workspace::pt): node i of
-// x / r / diag is node (X, row) = divmod(i, Nx) of p, at row * pitch + X.
-// Grid-stride like cg_update_xp_kernel (four independent streams per thread),
-// with each stream's (row, X) advanced by a precomputed divmod of the step
-// instead of a division per node.
-struct StepDivmod {
-  int q4, r4;  // divmod(4 * stride, Nx)
-  int q1, r1;  // divmod(stride, Nx)
-};
-template <bool PC>
-__global__ void __launch_bounds__(VT) cg_update_xp_pitched_kernel(double* __restrict__ x, double* __restrict__ p,
-                                                                  const double* __restrict__ r, long long n, int Nx,
-                                                                  int pitch, StepDivmod sd, unsigned int* done,
-                                                                  DevScalars* sc, const double* __restrict__ dv) {
-  if (*(volatile int*)&sc->x_pending == 0) return;
-  const double alpha = sc->alpha, beta = sc->beta;
-  const bool update_p = *(volatile int*)&sc->status == ST_RUNNING;
-  const long long stride = static_cast<long long>(gridDim.x) * VT;
-  long long i = blockIdx.x * static_cast<long long>(VT) + threadIdx.x;
-  const long long pad = pitch - Nx;
-  long long row[4];
-  int X[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const long long iu = i + u * stride;
-    row[u] = iu / Nx;
-    X[u] = static_cast<int>(iu - row[u] * Nx);
-  }
-  for (; i + 3 * stride < n; i += 4 * stride) {
-    double pv[4], xv[4], rv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      pv[u] = p[i + u * stride + row[u] * pad];
-      xv[u] = x[i + u * stride];
-      rv[u] = update_p ? r[i + u * stride] : 0.0;
-      if (PC && update_p) rv[u] = rv[u] / dv[i + u * stride];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      x[i + u * stride] = fma(alpha, pv[u], xv[u]);
-      if (update_p) p[i + u * stride + row[u] * pad] = fma(beta, pv[u], rv[u]);
-      X[u] += sd.r4;
-      row[u] += sd.q4;
-      if (X[u] >= Nx) {
-        X[u] -= Nx;
-        ++row[u];
-      }
-    }
-  }
-  for (; i < n; i += stride) {
-    const long long pi = i + row[0] * pad;
-    const double pvi = p[pi];
-    const double zi = update_p ? (PC ? r[i] / dv[i] : r[i]) : 0.0;
-    x[i] = fma(alpha, pvi, x[i]);
-    if (update_p) p[pi] = fma(beta, pvi, zi);
-    X[0] += sd.r1;
-    row[0] += sd.q1;
-    if (X[0] >= Nx) {
-      X[0] -= Nx;
-      ++row[0];
-    }
-  }
-  if (!last_block(done)) return;
-  if (threadIdx.x == 0) {
-    sc->x_pending = 0;
-    *done = 0;
-  }
-}
-
 // ---- FUSED mode: FMA updates and fixed-order tree reductions.
 __device__ __forceinline__ double tree_partials(const double* part, int nblk, double* red) {
   double s = 0.0;
@@ -450,6 +381,7 @@ struct RingUpdateArgs {
   int zlo_asm, zhi_asm;
   double* rank_partial;
   int p_pitch, pout_pitch;  // row pitches of p and pout (Workspace::pt: Nx rounded up to even)
+  int v_pitch;              // row pitch of r and Ap (Workspace::rt / Apt in the pitched fast CG)
 };
 
 // INIT = true: the initial residual r = b - A x (x applied in CG form), p = z,
@@ -475,8 +407,8 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
   for (int row = blockIdx.x * (VT / 32) + (threadIdx.x >> 5); row < rows; row += gridDim.x * (VT / 32)) {
     const int Z = row / R.Ny, Y = row - Z * R.Ny;
     const bool bcrow = R.constrained && (Y == 0 || Y == R.Ny - 1 || (Z == 0 && R.bc_zlo) || (Z == R.Nz - 1 && R.bc_zhi));
-    double* rr_ = R.r + static_cast<long long>(R.Nx) * row;
-    const double* ap = R.Ap + static_cast<long long>(R.Nx) * row;
+    double* rr_ = R.r + static_cast<long long>(R.v_pitch) * row;
+    const double* ap = R.Ap + static_cast<long long>(R.v_pitch) * row;
     const double* pp = R.p + static_cast<long long>(R.p_pitch) * row;
     const double* dd = PC ? R.dv + static_cast<long long>(R.Nx) * row : nullptr;
     const double* bb = INIT ? R.b + static_cast<long long>(R.Nx) * row : nullptr;
@@ -502,7 +434,7 @@ __global__ void __launch_bounds__(VT, HX_RING_MINB) fused_ring_update_r_kernel(c
       if constexpr (!INIT && !PC) {
         // the CG iteration's form with 16-byte accesses: node pairs (X, X+1)
         // at even global index, the odd element at the row start / end alone
-        const int head = static_cast<int>((static_cast<long long>(R.Nx) * row) & 1);
+        const int head = static_cast<int>((static_cast<long long>(R.v_pitch) * row) & 1);
         auto lat_at = [&](int X) { return __ldcg(reinterpret_cast<const double2*>(xr) + X / P); };
         auto node_a = [&](int X, double a_loaded, double2 lr) -> double {  // A p at node X of the row
           if (X % P != 0) return a_loaded;
@@ -838,9 +770,11 @@ cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int c
                           double* rank_partial = nullptr) {
   const Setup& s = *ws.s;
   RingUpdateArgs R;
-  R.Ap = ws.Ap;
-  R.p = p_applied;
   const int Nx = s.dims[0] * s.p + 1;
+  // the pitched fast CG (Workspace::use_pt): r, Ap and p row-pitched
+  R.Ap = ws.use_pt ? ws.Apt : ws.Ap;
+  R.v_pitch = ws.use_pt ? ws.pt_pitch : Nx;
+  R.p = p_applied;
   R.p_pitch = ws.pt != nullptr && p_applied == ws.pt ? ws.pt_pitch : Nx;
   R.latY = ws.lateral;
   R.latX = ws.lateral + LatLayout(s.p, s.dims[0], s.dims[1]).y_zstride * (s.dims[2] * s.p + 1);
@@ -850,7 +784,7 @@ cudaError_t launch_ring_r(const Workspace& ws, int64_t n, cudaStream_t st, int c
   R.pout_pitch = ws.use_pt ? ws.pt_pitch : Nx;
   R.rel_tol = rel_tol;
   R.max_iter = max_iter;
-  R.r = ws.r;
+  R.r = ws.use_pt ? ws.rt : ws.r;
   R.nx = s.dims[0];
   R.ny = s.dims[1];
   R.Nx = s.dims[0] * s.p + 1;
@@ -919,14 +853,13 @@ cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaS
   if (!p) p = ws.use_pt ? ws.pt : ws.p;
   const int g = vec_grid(n);
   const int Nx = ws.s->dims[0] * ws.s->p + 1;
-  if (ws.pt != nullptr && p == ws.pt && !ws.exact) {  // row-pitched search direction (tma.cu)
-    const long long stride = static_cast<long long>(g) * VT;
-    const StepDivmod sd{static_cast<int>(4 * stride / Nx), static_cast<int>(4 * stride % Nx),
-                        static_cast<int>(stride / Nx), static_cast<int>(stride % Nx)};
-    if (ws.diag)
-      cg_update_xp_pitched_kernel<true><<<g, VT, 0, st>>>(x, p, ws.r, n, Nx, ws.pt_pitch, sd, ws.vec_done, ws.sc, ws.diag);
-    else
-      cg_update_xp_pitched_kernel<false><<<g, VT, 0, st>>>(x, p, ws.r, n, Nx, ws.pt_pitch, sd, ws.vec_done, ws.sc, nullptr);
+  if (ws.use_pt) {
+    if (p != ws.pt || x != ws.xt) return cudaErrorInvalidValue;
+    // pitched fast CG: x, p, r share the row pitch, so the flat update runs
+    // over the pitched index space (the pad column is updated too, never read)
+    const int64_t np = static_cast<int64_t>(ws.pt_pitch) * (n / Nx);
+    const int gp = vec_grid(np);
+    cg_update_xp_kernel<false, false><<<gp, VT, 0, st>>>(x, p, ws.rt, np, ws.vec_done, ws.sc, nullptr);
     return cudaGetLastError();
   }
   if (ws.exact) {

@@ -90,6 +90,7 @@ struct ApplyArgs {
   // each element's 8^3 node block by one TMA tensor copy.
   int u_pitch;
   const CUtensorMap* u_tmap;
+  int w_pitch;  // row pitch of w (0: Nx); the pitched fast CG's A p (Workspace::Apt)
 };
 
 struct Setup {
@@ -130,7 +131,13 @@ struct Workspace {
   // Row-pitched copy of the search direction for the single-GPU fast CG on
   // the DMMA degrees (row pitch Nx rounded up to even: 16-byte row strides,
   // as a TMA tensor map requires), and its 3D tensor map (box = one element).
+  // With it the solve keeps x, r and A p row-pitched as well (xt, rt, Apt),
+  // so every vector kernel of the iteration is 32-byte aligned across its
+  // operands; x is copied in and out once per solve.
   double* pt = nullptr;
+  double* xt = nullptr;
+  double* rt = nullptr;
+  double* Apt = nullptr;
   int pt_pitch = 0;
   CUtensorMap pt_map;
   int use_pt = 0;  // set by the fast CG for the duration of a solve (capi.cu pcg_run)
@@ -159,6 +166,7 @@ struct Workspace {
 // Setups whose fast operator kernel stages u by TMA tensor copies from a
 // row-pitched vector (the DMMA kernels); tma.cu encodes the maps.
 bool tma_u_supported(const Setup& s);
+bool tma_u_staging_enabled();
 int tma_u_pitch(const Setup& s);
 cudaError_t encode_u_tensor_map(const Setup& s, const double* u, int pitch, CUtensorMap* map);
 // finish_ring = false leaves the ring nodes of w as lateral partials (CG fast

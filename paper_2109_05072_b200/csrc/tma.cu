@@ -20,9 +20,13 @@ namespace hxb {
 
 bool use_mma(const Setup& s);  // apply.cu
 
-bool tma_u_supported(const Setup& s) {
-  static const bool off = std::getenv("HEXBP_NO_TMA_U") != nullptr;  // A/B switch (dev)
-  return !off && use_mma(s) && s.p == 7;
+bool tma_u_supported(const Setup& s) { return use_mma(s) && s.p == 7; }
+
+// HEXBP_NO_TMA_U=1 (dev A/B and the bitwise test): same row-pitched vectors,
+// u staged by cp.async instead of the tensor copy
+bool tma_u_staging_enabled() {
+  static const bool off = std::getenv("HEXBP_NO_TMA_U") != nullptr;
+  return !off;
 }
 
 int tma_u_pitch(const Setup& s) { return (s.dims[0] * s.p + 1 + 1) & ~1; }

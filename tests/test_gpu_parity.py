@@ -174,8 +174,12 @@ def test_cg_matches_reference(golden_cg, name):
 # profiles/r2_parity_perturb.json); the reference-order reductions of
 # HEXBP_MODE_FAST_OPERATOR do not help (10 of 14 cases meet the bar there).
 # Their fast-mode deviations are deterministic and pinned here; only the
-# bit-exact reference mode (test_cg_matches_reference) can match them.
-FAST_EXCEPTIONS = {"bp3_p3_12_a0.1": (0, 1.5e-10), "bp5_p7_6_a0.1": (1, 2.5e-10)}
+# bit-exact reference mode (test_cg_matches_reference) can match them. Any
+# change of the fast path's rounding moves them: with the row-pitched vectors
+# of the DMMA degrees (tma.cu) the r.r partial sums pair nodes differently and
+# bp5_p7_6's final residual moved from 2.3e-10 to 5.2e-10 off the reference
+# (same 420-vs-419 iterations; profiles/r2s_parity_fast.json).
+FAST_EXCEPTIONS = {"bp3_p3_12_a0.1": (0, 1.5e-10), "bp5_p7_6_a0.1": (1, 6e-10)}
 
 
 @pytest.mark.parametrize("name", ["bp3_p3_12_a0.1", "bp3_p7_6_a0.1", "bp5_p7_6_a0.1", "bp1_p7_6_a0.1",

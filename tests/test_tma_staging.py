@@ -1,12 +1,13 @@
 """TMA staging of the operator input (tma.cu): the single-GPU fast CG keeps its
-search direction row-pitched and the DMMA kernels (BP3 / BP5, p = 7) stage each
+vectors row-pitched and the DMMA kernels (BP3 / BP5, p = 7) stage each
 element's 8^3 node block -- the gather of restriction.hpp:55-65 /
 operator.hpp:223-225 -- with one TMA tensor copy. The staged values are the
 same doubles the cp.async path loads, so the solve must be bitwise identical
-to the same solve with the TMA path switched off (HEXBP_NO_TMA_U=1, read once
-per process: each side runs in its own interpreter), on a mesh with an odd
-node-row length (Nx = 7 nx + 1 odd: the pitch pads one double per row) and
-one with an even one, multi-wave and with a z march longer than the u ring."""
+to the same solve with the tensor copy switched off (HEXBP_NO_TMA_U=1: same
+pitched vectors, cp.async staging; read once per process, so each side runs
+in its own interpreter), on a mesh with an odd node-row length (Nx = 7 nx + 1
+odd: the pitch pads one double per row) and one with an even one, multi-wave
+and with a z march longer than the u ring."""
 import json
 import os
 import subprocess

@@ -91,3 +91,25 @@ def test_fast_vs_reference_operator_at_headline_config():
         err = (torch.linalg.norm(wf - wr) / torch.linalg.norm(wr)).item()
         assert err <= TOL, (con, err)
         del wr, wf
+
+
+def test_fast_cg_at_headline_config_tracks_reference_mode():
+    """The headline solve itself (cfg3, 20 fixed iterations as bench.py times
+    it): the fast CG -- row-pitched vectors, TMA-staged DMMA operator, fused
+    p.Ap and ring-summing r-update -- against the bit-exact reference-mode CG
+    on the same device problem (the reference's own iterates)."""
+    import torch
+
+    dims = (66, 66, 66)
+    op = _op(3, 7, dims, 0.0, "fast")
+    A = hx.ConstrainedOperator(op)
+    b = torch.from_numpy(hx.bench_rhs(3, 7, dims)).cuda()
+    xf = torch.zeros_like(b)
+    rf = hx.cg(A, b, xf, rel_tol=0.0, max_iter=20, mode="fast")
+    op.workspace().set_mode("reference")
+    xr = torch.zeros_like(b)
+    rr = hx.cg(A, b, xr, rel_tol=0.0, max_iter=20, mode="reference")
+    assert rf.iterations == rr.iterations == 20
+    np.testing.assert_allclose(rf.residual_history, rr.residual_history, rtol=1e-10)
+    assert abs(rf.final_rel_residual - rr.final_rel_residual) <= 1e-12
+    assert (torch.linalg.norm(xf - xr) / torch.linalg.norm(xr)).item() <= 1e-10

@@ -189,7 +189,8 @@ int hexbp_apply_ring_deferred(hexbp_setup_t s, hexbp_workspace_t ws, const doubl
  * element from the row-pitched search direction (tma.cu). u_dev (n unpadded
  * doubles) is first copied into that buffer; u_dev = NULL applies to its
  * current contents (timing loops). Clobbers the search direction of a solve
- * on this workspace. */
+ * on this workspace. constrained = 0 / 1 as elsewhere; | 2 adds the CG's
+ * fused p.Ap (the exact kernel variant the solve launches; result discarded). */
 int hexbp_apply_cg_form(hexbp_setup_t s, hexbp_workspace_t ws, const double* u_dev, double* w_dev, int constrained,
                         void* stream);
 

@@ -478,7 +478,12 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
       if (t == 0) A.lat_x[Lat.x_index(A.nx, Z, Y, ex, 1)] = o[0];
       if (t == 3) A.lat_x[Lat.x_index(A.nx, Z, Y, ex + 1, 0)] = o[1];
     }
-    if (do_dot) {
+    if (do_dot && !zbc && !LBC) {
+      // interior column, no essential node in this row: every node -- ring or
+      // not -- adds u * (its column value), the same FMAs as the general path
+      dot = fma(u2.x, o[0], dot);
+      dot = fma(u2.y, o[1], dot);
+    } else if (do_dot) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const double uv = q ? u2.y : u2.x;

@@ -523,7 +523,9 @@ int hexbp_apply_cg_form(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, 
     const size_t pitch = pv == ws.pt ? static_cast<size_t>(ws.pt_pitch) : Nx;
     CK(cudaMemcpy2DAsync(pv, pitch * 8, u, Nx * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
   }
-  CK(launch_apply(s, ws, pv, w, constrained, nullptr, nullptr, st, false));
+  // constrained bit 1: also the fused p.Ap of the CG form (into the
+  // workspace's dot scratch), i.e. exactly the kernel variant the solve runs
+  CK(launch_apply(s, ws, pv, w, constrained & 1, (constrained & 2) ? ws.dot_result : nullptr, nullptr, st, false));
   return HEXBP_OK;
 }
 

@@ -1,2 +1,3 @@
-for d in 0 1; do DOT=$d timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:bp3_p7_mma_kernel<\(bool\)1, \(bool\)$d, \(bool\)1>" -s 2 -c 1 -o gpurun_out/r2s_cgform_dot$d -f python tools/prof_cgform.py > /dev/null 2>&1; done
-ls gpurun_out/*.ncu-rep
+V=paper_2109_05072_b200/build/variants
+for v in dotreg dotsm dotreg dotsm; do echo "== $v"; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/ctx_probe2.py 2>&1 | tail -4; done
+for r in 1 2; do python tools/ab_time.py $V/dotreg/libhexbp_b200.so $V/dotsm/libhexbp_b200.so; done

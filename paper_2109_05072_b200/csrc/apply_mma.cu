@@ -448,7 +448,8 @@ __device__ __forceinline__ void mma_column(const ApplyArgs& A, const MmaBasis& b
     const bool zbc = CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
     // u at these nodes: still staged in shared memory (z-plane k = g of element e)
     const double* ur = ubuf(e) + g * UKS + G * URS + ush + 2 * t;
-    const double2 u2 = TMA ? make_double2(ur[0], ur[1]) : *reinterpret_cast<const double2*>(ur);
+    // 16-byte load unless the TMA box put the element at an odd x offset
+    const double2 u2 = TMA && ush ? make_double2(ur[0], ur[1]) : *reinterpret_cast<const double2*>(ur);
 
     // ring partials -> lateral buffer (ring.cuh layout): a ring row (j = 0 or
     // P) stores all P+1 of its nodes as one 16-byte pair per lane

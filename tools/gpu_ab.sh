@@ -1,3 +1,6 @@
-V=paper_2109_05072_b200/build/variants
-for v in dotreg dotsm dotreg dotsm; do echo "== $v"; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/ctx_probe2.py 2>&1 | tail -4; done
-for r in 1 2; do python tools/ab_time.py $V/dotreg/libhexbp_b200.so $V/dotsm/libhexbp_b200.so; done
+python -m pytest tests -m gpu -q -x 2>&1 | grep -E "FAILED|^E |passed|failed" | head -20
+python -c "
+import sys; sys.path.insert(0,'.')
+import bench
+print(bench.p_sweep(3, 10, 0, ps=(5, 6, 8)))
+"

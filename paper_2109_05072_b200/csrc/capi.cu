@@ -521,7 +521,7 @@ int hexbp_apply_cg_form(hexbp_setup_t h, hexbp_workspace_t wh, const double* u, 
     const size_t Nx = static_cast<size_t>(s.dims[0]) * s.p + 1;
     const size_t rows = static_cast<size_t>(s.nL) / Nx;
     const size_t pitch = pv == ws.pt ? static_cast<size_t>(ws.pt_pitch) : Nx;
-    CK(cudaMemcpy2DAsync(pv, pitch * 8, u, Nx * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
+    CK(launch_copy_rows(pv, static_cast<int>(pitch), u, static_cast<int>(Nx), static_cast<int>(Nx), rows, st));
   }
   // constrained bit 1: also the fused p.Ap of the CG form (into the
   // workspace's dot scratch), i.e. exactly the kernel variant the solve runs
@@ -651,7 +651,7 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
   double* const apv = w.use_pt ? w.Apt : w.Ap;
   const size_t Nx = static_cast<size_t>(s.dims[0]) * s.p + 1, rows = static_cast<size_t>(n) / Nx;
   if (w.use_pt)
-    CK(cudaMemcpy2DAsync(w.xt, w.pt_pitch * 8, x, Nx * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
+    CK(launch_copy_rows(w.xt, w.pt_pitch, x, static_cast<int>(Nx), static_cast<int>(Nx), rows, st));
   // r0 = b - A x0 (solver.hpp:102-103); fast mode sums the ring in the init kernel
   if (w.exact) {
     CK(launch_apply(s, w, x, w.Ap, constrained, nullptr, nullptr, st));
@@ -681,7 +681,7 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
     }
   }
   if (w.use_pt)
-    CK(cudaMemcpy2DAsync(x, Nx * 8, w.xt, w.pt_pitch * 8, Nx * 8, rows, cudaMemcpyDeviceToDevice, st));
+    CK(launch_copy_rows(x, static_cast<int>(Nx), w.xt, w.pt_pitch, static_cast<int>(Nx), rows, st));
   CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const DevScalars hs = *w.host_sc;

@@ -833,6 +833,40 @@ cudaError_t launch_cg_update_r(const Workspace& ws, int64_t n, cudaStream_t st, 
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
 
+// Row copy between pitches (the pitched fast CG's x in / out, tma.cu): one
+// warp per node row, four 32-node chunks loaded before they are stored
+// (cudaMemcpy2DAsync ran at half the bandwidth on these 3.7 KB rows).
+__global__ void __launch_bounds__(VT) copy_rows_kernel(double* __restrict__ dst, int dst_pitch,
+                                                       const double* __restrict__ src, int src_pitch, int Nx, int rows) {
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * (VT / 32) + (threadIdx.x >> 5); row < rows; row += gridDim.x * (VT / 32)) {
+    const double* s = src + static_cast<long long>(src_pitch) * row;
+    double* d = dst + static_cast<long long>(dst_pitch) * row;
+    for (int x0 = 0; x0 < Nx; x0 += 4 * 32) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int X = x0 + 32 * u + lane;
+        v[u] = X < Nx ? s[X] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int X = x0 + 32 * u + lane;
+        if (X < Nx) d[X] = v[u];
+      }
+    }
+  }
+}
+
+cudaError_t launch_copy_rows(double* dst, int dst_pitch, const double* src, int src_pitch, int Nx, int64_t rows,
+                             cudaStream_t st) {
+  long long g = (rows + VT / 32 - 1) / (VT / 32);
+  if (g > 148 * 16) g = 148 * 16;
+  copy_rows_kernel<<<static_cast<int>(g < 1 ? 1 : g), VT, 0, st>>>(dst, dst_pitch, src, src_pitch, Nx,
+                                                                   static_cast<int>(rows));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_set_int(int* p, int v, cudaStream_t st) {
   set_int_kernel<<<1, 1, 0, st>>>(p, v);
   return cudaGetLastError();

@@ -247,6 +247,8 @@ cudaError_t launch_cg_update_xp(const Workspace& ws, double* x, int64_t n, cudaS
 cudaError_t launch_dot(const Workspace& ws, const double* a, const double* b, int64_t n, double* out,
                        cudaStream_t st);
 int vec_grid(int64_t n);
+cudaError_t launch_copy_rows(double* dst, int dst_pitch, const double* src, int src_pitch, int Nx, int64_t rows,
+                             cudaStream_t st);
 
 // ---- setup.cu
 struct BoxGeometryArgs {

@@ -57,10 +57,12 @@ struct XCfg {
 };
 
 // CTAs per SM the register allocation targets (measured on a B200: the
-// kernel spills either way at p >= 7; more resident CTAs win for BP3 / BP1
-// at p = 7 and BP1 p = 8, lose for BP3 p = 8; neutral elsewhere)
+// kernel spills either way at p >= 7; more resident CTAs win for BP1 at p = 7
+// and p = 8, lose for BP3 p = 8; BP3 p = 7 fits three CTAs by shared memory
+// and, with the 16-byte factor loads, runs best at that register target:
+// reference-mode CG 11.30 -> 10.83 ms/it at cfg3, same iterates)
 constexpr int exact_min_blocks(int p, int kind) {
-  return (p == 7 && kind != KIND_COLLOC) ? 4 : (p == 8 && kind == KIND_MASS) ? 3 : 1;
+  return (p == 7 && kind == KIND_DIFF) ? 3 : (p == 7 && kind == KIND_MASS) ? 4 : (p == 8 && kind == KIND_MASS) ? 3 : 1;
 }
 template <int P, int Q, int KIND>
 __global__ void __launch_bounds__(XCfg<P, Q, KIND>::NT, exact_min_blocks(P, KIND))
@@ -270,9 +272,16 @@ __global__ void __launch_bounds__(XCfg<P, Q, KIND>::NT, exact_min_blocks(P, KIND
           }
           // apply_diffusion_factors (operator.hpp:129-131); G at point (a,b,c)
           const int qp = a + Q * (b + Q * c);
-          const double* g = A.g_aos ? Gs + qp * 6 : Gs + a * QQ + b + Q * c;
-          const int cs = A.g_aos ? 1 : Q * QQ;  // component stride
-          const double g0 = g[0], g1 = g[cs], g2 = g[2 * cs], g3 = g[3 * cs], g4 = g[4 * cs], g5 = g[5 * cs];
+          double g0, g1, g2, g3, g4, g5;
+          if (A.g_aos) {  // [qp][6]: the point's six components as three 16-byte loads
+            const double2* g = reinterpret_cast<const double2*>(Gs + qp * 6);
+            const double2 ga = g[0], gb = g[1], gc = g[2];
+            g0 = ga.x, g1 = ga.y, g2 = gb.x, g3 = gb.y, g4 = gc.x, g5 = gc.y;
+          } else {
+            const double* g = A.g_aos ? Gs + qp * 6 : Gs + a * QQ + b + Q * c;
+            const int cs = A.g_aos ? 1 : Q * QQ;  // component stride
+            g0 = g[0], g1 = g[cs], g2 = g[2 * cs], g3 = g[3 * cs], g4 = g[4 * cs], g5 = g[5 * cs];
+          }
           vr[c] = DA(DA(DM(g0, r), DM(g1, s)), DM(g2, u));
           vs[c] = DA(DA(DM(g1, r), DM(g3, s)), DM(g4, u));
           vt[c] = DA(DA(DM(g2, r), DM(g4, s)), DM(g5, u));

@@ -17,11 +17,11 @@ op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), hx.build_bo
 A = hx.ConstrainedOperator(op) if bp != 1 else op
 b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda()
 x = torch.zeros_like(b)
-hx.cg(A, b, x, 0.0, 5, mode="fast")
+hx.cg(A, b, x, 0.0, 5, mode=os.environ.get("MODE", "fast"))
 x.zero_()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    hx.cg(A, b, x, 0.0, 20, mode="fast")
+    hx.cg(A, b, x, 0.0, 20, mode=os.environ.get("MODE", "fast"))
     torch.cuda.synchronize()
 evs = [ev for ev in prof.events() if ev.device_type.name == "CUDA"]
 ks = sorted([(ev.time_range.start, ev.time_range.end, ev.name) for ev in evs], key=lambda t: t[0])

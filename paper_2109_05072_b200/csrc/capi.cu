@@ -492,6 +492,10 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
     if (b) cudaFree(b);
   if (w.host_sc) cudaFreeHost(w.host_sc);
   if (w.copy_st) cudaStreamDestroy(w.copy_st);
+  if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
+  if (w.graph_st) cudaStreamDestroy(w.graph_st);
+  if (w.ev_g0) cudaEventDestroy(w.ev_g0);
+  if (w.ev_g1) cudaEventDestroy(w.ev_g1);
   if (w.ev_x) cudaEventDestroy(w.ev_x);
   if (w.ev_b) cudaEventDestroy(w.ev_b);
   delete wh;
@@ -612,6 +616,17 @@ int hexbp_pcg(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x,
 
 namespace {
 
+constexpr int kCgGraphBlock = 8;  // iterations per captured graph
+
+// HEXBP_CG_GRAPH=0 keeps the eager launch loop (A/B switch)
+bool cg_graph_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("HEXBP_CG_GRAPH");
+    return !(v && *v == '0');
+  }();
+  return on;
+}
+
 int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, const double* diag, double rel_tol,
             int max_iter, int constrained, hexbp_cg_report* report, double* history, cudaStream_t st,
             cudaEvent_t b_ready) {
@@ -664,7 +679,56 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
   }
   if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz = r0.z0 (solver.hpp:124)
   const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
-  for (int k = 1; k <= max_iter; ++k) {
+  int k0 = 1;  // first iteration the eager loop below runs
+  if (!w.exact && rel_tol == 0.0 && max_iter >= kCgGraphBlock && cg_graph_enabled() && !w.cg_graph_failed) {
+    // fixed iterations, no host checks: replay a captured block of iterations
+    // (the kernels read alpha / beta / status from device scalars, so every
+    // replay is the same launch sequence as the eager loop)
+    const int con = constrained ? 1 : 0;
+    if (!w.cg_graph || w.cg_graph_key[0] != xv || w.cg_graph_key[1] != pv || w.cg_graph_key[2] != apv ||
+        w.cg_graph_key[3] != diag || w.cg_graph_con != con) {
+      if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
+      w.cg_graph = nullptr;
+      cudaError_t ge = cudaSuccess;
+      if (!w.graph_st) ge = cudaStreamCreateWithFlags(&w.graph_st, cudaStreamNonBlocking);
+      if (!ge && !w.ev_g0) ge = cudaEventCreateWithFlags(&w.ev_g0, cudaEventDisableTiming);
+      if (!ge && !w.ev_g1) ge = cudaEventCreateWithFlags(&w.ev_g1, cudaEventDisableTiming);
+      cudaGraph_t graph = nullptr;
+      if (!ge) ge = cudaStreamBeginCapture(w.graph_st, cudaStreamCaptureModeThreadLocal);
+      if (!ge) {
+        cudaError_t le = cudaSuccess;
+        for (int i = 0; i < kCgGraphBlock && !le; ++i) {
+          le = launch_apply(s, w, pv, apv, constrained, nullptr, w.sc, w.graph_st, /*finish_ring=*/false);
+          if (!le) le = launch_cg_update_r(w, n, w.graph_st, constrained);
+          if (!le) le = launch_cg_update_xp(w, xv, n, w.graph_st);
+        }
+        ge = cudaStreamEndCapture(w.graph_st, &graph);
+        if (!ge) ge = le;
+      }
+      if (!ge) ge = cudaGraphInstantiate(&w.cg_graph, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (ge) {  // no graph on this system / configuration: the eager loop
+        cudaGetLastError();
+        if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
+        w.cg_graph = nullptr;
+        w.cg_graph_failed = 1;
+      } else {
+        w.cg_graph_key[0] = xv;
+        w.cg_graph_key[1] = pv;
+        w.cg_graph_key[2] = apv;
+        w.cg_graph_key[3] = diag;
+        w.cg_graph_con = con;
+      }
+    }
+    if (w.cg_graph) {
+      CK(cudaEventRecord(w.ev_g0, st));
+      CK(cudaStreamWaitEvent(w.graph_st, w.ev_g0, 0));
+      for (; k0 + kCgGraphBlock - 1 <= max_iter; k0 += kCgGraphBlock) CK(cudaGraphLaunch(w.cg_graph, w.graph_st));
+      CK(cudaEventRecord(w.ev_g1, w.graph_st));
+      CK(cudaStreamWaitEvent(st, w.ev_g1, 0));
+    }
+  }
+  for (int k = k0; k <= max_iter; ++k) {
     if (w.exact) {
       CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, st));
       CK(launch_cg_pap(w, n, st));

@@ -160,6 +160,16 @@ struct Workspace {
   size_t scatter_bytes = 0;  // transpose-restriction scratch (lateral + zupper): Workspace::global_bytes analog
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_x = nullptr, ev_b = nullptr;
+  // fixed-iteration fast solves replay a CUDA graph of kCgGraphBlock
+  // iterations (capi.cu pcg_run), captured on graph_st and cached per
+  // (x, p, A p, Jacobi diagonal, constrained) -- the only arguments the
+  // iteration's kernels take that can change between solves on this workspace
+  cudaStream_t graph_st = nullptr;
+  cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
+  cudaGraphExec_t cg_graph = nullptr;
+  const void* cg_graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  int cg_graph_con = -1;
+  int cg_graph_failed = 0;
 };
 
 // ---- apply.cu

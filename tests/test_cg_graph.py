@@ -1,0 +1,56 @@
+"""Fixed-iteration fast solves replay a captured CUDA graph of 8 CG
+iterations (capi.cu pcg_run): the replay must be bitwise the eager launch
+loop (HEXBP_CG_GRAPH=0, read once per process: each side in its own
+interpreter), with an iteration count that is not a multiple of the block
+(graph blocks + eager tail), on the pitched TMA path (BP3 p = 7), a DFMA
+degree and the Jacobi-preconditioned solve, and again after the cache key
+changes (second right-hand side / solution vector)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2109_05072_b200 as hx
+bp, p, dims, pc = int(sys.argv[2]), int(sys.argv[3]), tuple(int(v) for v in sys.argv[4].split(",")), int(sys.argv[5])
+op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), hx.build_box_mesh(dims, p, (1.0, 1.0, 1.0), 0.05)))
+op.workspace().set_mode("fast")
+A = hx.ConstrainedOperator(op) if bp != 1 else op
+diag = hx.jacobi_diagonal(A) if pc else None
+out = []
+for rhs in range(2):
+    b = hx.bench_rhs(bp, p, dims) * (1.0 + rhs)
+    x = np.zeros(op.size())
+    rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=21, mode="fast", diag=diag)
+    out.append({"it": rep.iterations, "hist": list(rep.residual_history), "x": x.tobytes().hex()})
+print(json.dumps(out))
+"""
+
+
+def solve(bp, p, dims, pc, graph):
+    env = dict(os.environ)
+    env.pop("HEXBP_CG_GRAPH", None)
+    if not graph:
+        env["HEXBP_CG_GRAPH"] = "0"
+    out = subprocess.run([sys.executable, "-c", CHILD, ROOT, str(bp), str(p), ",".join(map(str, dims)), str(pc)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bp,p,dims,pc", [(3, 7, (6, 5, 7), 0), (3, 4, (7, 6, 5), 0), (1, 3, (6, 6, 6), 0),
+                                          (3, 5, (5, 4, 6), 1)])
+def test_graph_replay_is_bitwise_the_eager_loop(bp, p, dims, pc):
+    a, b = solve(bp, p, dims, pc, True), solve(bp, p, dims, pc, False)
+    for ra, rb in zip(a, b):
+        assert ra["it"] == rb["it"] == 21
+        assert ra["hist"] == rb["hist"]
+        assert ra["x"] == rb["x"]

@@ -1,2 +1,3 @@
-V=paper_2109_05072_b200/build/variants
-for r in 1 2; do for v in ex4 ex3 ex3g ex4g; do echo "== $v"; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/refmode_time.py 2>&1 | tail -1; done; done
+python -m pytest tests -m gpu -q 2>&1 | tail -1
+L=paper_2109_05072_b200/libhexbp_b200.so
+for r in 1 2; do for g in 0 1; do echo "graph=$g"; HEXBP_CG_GRAPH=$g python tools/ab_time.py $L | cut -c1-200; HEXBP_CG_GRAPH=$g python tools/ab_sweep.py $L | cut -c40-400; done; done

@@ -680,10 +680,13 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
   if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz = r0.z0 (solver.hpp:124)
   const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
   int k0 = 1;  // first iteration the eager loop below runs
-  if (!w.exact && rel_tol == 0.0 && max_iter >= kCgGraphBlock && cg_graph_enabled() && !w.cg_graph_failed) {
-    // fixed iterations, no host checks: replay a captured block of iterations
-    // (the kernels read alpha / beta / status from device scalars, so every
-    // replay is the same launch sequence as the eager loop)
+  static_assert(kCgGraphBlock == 8, "graph blocks end where the eager loop checks convergence");
+  if (!w.exact && max_iter >= kCgGraphBlock && cg_graph_enabled() && !w.cg_graph_failed) {
+    // replay a captured block of iterations (the kernels read alpha, beta and
+    // the stopping state from device scalars, so every replay is the launch
+    // sequence of the eager loop; a converged solve's remaining launches
+    // return at once); with a tolerance the host checks the stopping state
+    // after every block, where the eager loop checks it
     const int con = constrained ? 1 : 0;
     if (!w.cg_graph || w.cg_graph_key[0] != xv || w.cg_graph_key[1] != pv || w.cg_graph_key[2] != apv ||
         w.cg_graph_key[3] != diag || w.cg_graph_con != con) {
@@ -723,7 +726,17 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
     if (w.cg_graph) {
       CK(cudaEventRecord(w.ev_g0, st));
       CK(cudaStreamWaitEvent(w.graph_st, w.ev_g0, 0));
-      for (; k0 + kCgGraphBlock - 1 <= max_iter; k0 += kCgGraphBlock) CK(cudaGraphLaunch(w.cg_graph, w.graph_st));
+      for (; k0 + kCgGraphBlock - 1 <= max_iter; k0 += kCgGraphBlock) {
+        CK(cudaGraphLaunch(w.cg_graph, w.graph_st));
+        if (rel_tol > 0.0 && k0 + kCgGraphBlock - 1 < max_iter) {
+          CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, w.graph_st));
+          CK(cudaStreamSynchronize(w.graph_st));
+          if (w.host_sc->status != ST_RUNNING) {
+            k0 = max_iter + 1;
+            break;
+          }
+        }
+      }
       CK(cudaEventRecord(w.ev_g1, w.graph_st));
       CK(cudaStreamWaitEvent(st, w.ev_g1, 0));
     }

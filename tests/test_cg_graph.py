@@ -4,7 +4,8 @@ loop (HEXBP_CG_GRAPH=0, read once per process: each side in its own
 interpreter), with an iteration count that is not a multiple of the block
 (graph blocks + eager tail), on the pitched TMA path (BP3 p = 7), a DFMA
 degree and the Jacobi-preconditioned solve, and again after the cache key
-changes (second right-hand side / solution vector)."""
+changes (second right-hand side / solution vector); and solves to a
+tolerance, where the host checks the stopping state after every block."""
 import json
 import os
 import subprocess
@@ -30,6 +31,9 @@ for rhs in range(2):
     x = np.zeros(op.size())
     rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=21, mode="fast", diag=diag)
     out.append({"it": rep.iterations, "hist": list(rep.residual_history), "x": x.tobytes().hex()})
+    x = np.zeros(op.size())  # to tolerance: blocks with a host check after each
+    rep = hx.cg(A, b, x, rel_tol=1e-9, max_iter=2000, mode="fast", diag=diag)
+    out.append({"it": rep.iterations, "hist": list(rep.residual_history), "x": x.tobytes().hex()})
 print(json.dumps(out))
 """
 
@@ -50,7 +54,7 @@ def solve(bp, p, dims, pc, graph):
                                           (3, 5, (5, 4, 6), 1)])
 def test_graph_replay_is_bitwise_the_eager_loop(bp, p, dims, pc):
     a, b = solve(bp, p, dims, pc, True), solve(bp, p, dims, pc, False)
-    for ra, rb in zip(a, b):
-        assert ra["it"] == rb["it"] == 21
+    for k, (ra, rb) in enumerate(zip(a, b)):
+        assert ra["it"] == rb["it"] and (ra["it"] == 21 if k % 2 == 0 else ra["it"] > 21)
         assert ra["hist"] == rb["hist"]
         assert ra["x"] == rb["x"]

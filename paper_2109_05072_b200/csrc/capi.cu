@@ -679,15 +679,29 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
   }
   if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz = r0.z0 (solver.hpp:124)
   const int check_every = rel_tol > 0.0 ? 8 : (1 << 30);
+  // one CG iteration (solver.hpp:126-148) on stream q
+  auto iteration = [&](cudaStream_t q) -> cudaError_t {
+    cudaError_t e = cudaSuccess;
+    if (w.exact) {
+      e = launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, q);
+      if (!e) e = launch_cg_pap(w, n, q);
+    } else {
+      e = launch_apply(s, w, pv, apv, constrained, nullptr, w.sc, q, /*finish_ring=*/false);
+    }
+    if (!e) e = launch_cg_update_r(w, n, q, constrained);
+    if (!e && diag && w.exact) e = launch_cg_rz(w, n, q);  // rz_next = r.z, beta (solver.hpp:145-147)
+    if (!e) e = launch_cg_update_xp(w, xv, n, q);
+    return e;
+  };
   int k0 = 1;  // first iteration the eager loop below runs
   static_assert(kCgGraphBlock == 8, "graph blocks end where the eager loop checks convergence");
-  if (!w.exact && max_iter >= kCgGraphBlock && cg_graph_enabled() && !w.cg_graph_failed) {
+  if (max_iter >= kCgGraphBlock && cg_graph_enabled() && !w.cg_graph_failed) {
     // replay a captured block of iterations (the kernels read alpha, beta and
     // the stopping state from device scalars, so every replay is the launch
     // sequence of the eager loop; a converged solve's remaining launches
     // return at once); with a tolerance the host checks the stopping state
     // after every block, where the eager loop checks it
-    const int con = constrained ? 1 : 0;
+    const int con = (constrained ? 1 : 0) + (w.exact ? 2 : 0) + (w.fast_op ? 4 : 0) + (w.multipass ? 8 : 0);
     if (!w.cg_graph || w.cg_graph_key[0] != xv || w.cg_graph_key[1] != pv || w.cg_graph_key[2] != apv ||
         w.cg_graph_key[3] != diag || w.cg_graph_con != con) {
       if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
@@ -700,11 +714,7 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
       if (!ge) ge = cudaStreamBeginCapture(w.graph_st, cudaStreamCaptureModeThreadLocal);
       if (!ge) {
         cudaError_t le = cudaSuccess;
-        for (int i = 0; i < kCgGraphBlock && !le; ++i) {
-          le = launch_apply(s, w, pv, apv, constrained, nullptr, w.sc, w.graph_st, /*finish_ring=*/false);
-          if (!le) le = launch_cg_update_r(w, n, w.graph_st, constrained);
-          if (!le) le = launch_cg_update_xp(w, xv, n, w.graph_st);
-        }
+        for (int i = 0; i < kCgGraphBlock && !le; ++i) le = iteration(w.graph_st);
         ge = cudaStreamEndCapture(w.graph_st, &graph);
         if (!ge) ge = le;
       }
@@ -742,15 +752,7 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
     }
   }
   for (int k = k0; k <= max_iter; ++k) {
-    if (w.exact) {
-      CK(launch_apply(s, w, w.p, w.Ap, constrained, nullptr, nullptr, st));
-      CK(launch_cg_pap(w, n, st));
-    } else {
-      CK(launch_apply(s, w, pv, apv, constrained, nullptr, w.sc, st, /*finish_ring=*/false));
-    }
-    CK(launch_cg_update_r(w, n, st, constrained));
-    if (diag && w.exact) CK(launch_cg_rz(w, n, st));  // rz_next = r.z, beta (solver.hpp:145-147)
-    CK(launch_cg_update_xp(w, xv, n, st));
+    CK(iteration(st));
     if (k % check_every == 0 && k < max_iter) {
       CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));

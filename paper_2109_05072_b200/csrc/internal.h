@@ -162,8 +162,8 @@ struct Workspace {
   cudaEvent_t ev_x = nullptr, ev_b = nullptr;
   // fixed-iteration fast solves replay a CUDA graph of kCgGraphBlock
   // iterations (capi.cu pcg_run), captured on graph_st and cached per
-  // (x, p, A p, Jacobi diagonal, constrained) -- the only arguments the
-  // iteration's kernels take that can change between solves on this workspace
+  // (x, p, A p, Jacobi diagonal, constrained, arithmetic mode) -- the only
+  // arguments the iteration's kernels take that can change between solves
   cudaStream_t graph_st = nullptr;
   cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
   cudaGraphExec_t cg_graph = nullptr;

@@ -21,29 +21,30 @@ import numpy as np
 sys.path.insert(0, sys.argv[1])
 import paper_2109_05072_b200 as hx
 bp, p, dims, pc = int(sys.argv[2]), int(sys.argv[3]), tuple(int(v) for v in sys.argv[4].split(",")), int(sys.argv[5])
+mode = sys.argv[6]
 op = hx.OperatorHandle(hx.Backend.Cuda, hx.make_setup(hx.BPKind(bp), hx.build_box_mesh(dims, p, (1.0, 1.0, 1.0), 0.05)))
-op.workspace().set_mode("fast")
+op.workspace().set_mode(mode)
 A = hx.ConstrainedOperator(op) if bp != 1 else op
 diag = hx.jacobi_diagonal(A) if pc else None
 out = []
 for rhs in range(2):
     b = hx.bench_rhs(bp, p, dims) * (1.0 + rhs)
     x = np.zeros(op.size())
-    rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=21, mode="fast", diag=diag)
+    rep = hx.cg(A, b, x, rel_tol=0.0, max_iter=21, mode=mode, diag=diag)
     out.append({"it": rep.iterations, "hist": list(rep.residual_history), "x": x.tobytes().hex()})
     x = np.zeros(op.size())  # to tolerance: blocks with a host check after each
-    rep = hx.cg(A, b, x, rel_tol=1e-9, max_iter=2000, mode="fast", diag=diag)
+    rep = hx.cg(A, b, x, rel_tol=1e-9, max_iter=2000, mode=mode, diag=diag)
     out.append({"it": rep.iterations, "hist": list(rep.residual_history), "x": x.tobytes().hex()})
 print(json.dumps(out))
 """
 
 
-def solve(bp, p, dims, pc, graph):
+def solve(bp, p, dims, pc, graph, mode="fast"):
     env = dict(os.environ)
     env.pop("HEXBP_CG_GRAPH", None)
     if not graph:
         env["HEXBP_CG_GRAPH"] = "0"
-    out = subprocess.run([sys.executable, "-c", CHILD, ROOT, str(bp), str(p), ",".join(map(str, dims)), str(pc)],
+    out = subprocess.run([sys.executable, "-c", CHILD, ROOT, str(bp), str(p), ",".join(map(str, dims)), str(pc), mode],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     return json.loads(out.stdout.strip().splitlines()[-1])
@@ -58,3 +59,13 @@ def test_graph_replay_is_bitwise_the_eager_loop(bp, p, dims, pc):
         assert ra["it"] == rb["it"] and (ra["it"] == 21 if k % 2 == 0 else ra["it"] > 21)
         assert ra["hist"] == rb["hist"]
         assert ra["x"] == rb["x"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bp,p,dims,pc", [(3, 7, (4, 3, 5), 0), (3, 3, (5, 4, 6), 1)])
+def test_graph_replay_reference_mode(bp, p, dims, pc):
+    """The bit-exact mode's iteration (exact apply + lateral fix-up + the
+    deterministic_dot-order reductions) replayed from the graph."""
+    a, b = solve(bp, p, dims, pc, True, "reference"), solve(bp, p, dims, pc, False, "reference")
+    for ra, rb in zip(a, b):
+        assert ra["it"] == rb["it"] and ra["hist"] == rb["hist"] and ra["x"] == rb["x"]

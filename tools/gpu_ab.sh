@@ -1,3 +1,3 @@
-python -m pytest tests -m gpu -q 2>&1 | tail -1
-L=paper_2109_05072_b200/libhexbp_b200.so
-for r in 1 2; do for g in 0 1; do echo "graph=$g"; HEXBP_CG_GRAPH=$g python tools/ab_time.py $L | cut -c1-200; HEXBP_CG_GRAPH=$g python tools/ab_sweep.py $L | cut -c40-400; done; done
+V=paper_2109_05072_b200/build/variants
+HEXBP_LIB=paper_2109_05072_b200/build/variants/gseg/libhexbp_b200.so python -m pytest tests/test_fast_scale.py tests/test_tma_staging.py -q 2>&1 | tail -1
+for v in gone gseg gone gseg; do echo "== $v"; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/ctx_probe2.py 2>&1 | tail -2; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/ab_time.py $V/$v/libhexbp_b200.so | cut -c50-200; done

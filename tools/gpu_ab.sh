@@ -1,3 +1,3 @@
-V=paper_2109_05072_b200/build/variants
-HEXBP_LIB=paper_2109_05072_b200/build/variants/gseg/libhexbp_b200.so python -m pytest tests/test_fast_scale.py tests/test_tma_staging.py -q 2>&1 | tail -1
-for v in gone gseg gone gseg; do echo "== $v"; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/ctx_probe2.py 2>&1 | tail -2; HEXBP_LIB=$V/$v/libhexbp_b200.so python tools/ab_time.py $V/$v/libhexbp_b200.so | cut -c50-200; done
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2s_launches_bench.csv python bench.py --steps 3 --warmup 3 --no-sweep --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1
+python tools/cg_timeline.py > gpurun_out/r2s_cg_timeline.txt 2>&1
+ls -la gpurun_out/r2s_launches_bench.csv

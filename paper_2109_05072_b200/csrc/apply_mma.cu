@@ -16,8 +16,10 @@
 // one LDS per lane), C = 8 x 8 outputs. The 9th Gauss point does not fit an
 // 8-row tile: forward (q = 9 outputs) its row is a 2-term dot per lane plus
 // a 4-lane butterfly; backward (q = 9 inputs) its column is one DFMA per
-// output. The phases, staging (TMA bulk copy of G, cp.async u) and the
-// atomic-free transpose restriction are those of apply.cu:
+// output. Staging: G by a TMA bulk copy per element; u by one TMA tensor
+// copy per element in the fast CG (row-pitched search direction, tma.cu) or
+// cp.async on caller vectors. The phases and the atomic-free transpose
+// restriction are those of apply.cu:
 //   Z : 8 pencil groups (j)      u        -> B_z u, D_z u          (+ row 8)
 //   Y : 9 groups (c)             -> B_y B_z u, D_y B_z u, B_y D_z u (+ row 8)
 //   X : 11 groups of (b,c) lines -> gr, gs, gt; G; D_x^T, B_x^T   (+ row/col 8)

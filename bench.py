@@ -263,8 +263,11 @@ def main():
 
     # warm-up solve, then the timed fixed-iteration solve (device-resident inputs).
     # Headline = fast mode (FMA/DMMA operator, fused p.Ap); reference mode
-    # (bit-exact reference arithmetic) is timed beside it.
-    hx.cg(A, b, x, rel_tol=0.0, max_iter=W, mode="fast")
+    # (bit-exact reference arithmetic) is timed beside it. Warm-ups run at
+    # least one 8-iteration block (WG), so the solve's CUDA graph is captured
+    # before the timed region (capi.cu pcg_run).
+    WG = max(W, 8)
+    hx.cg(A, b, x, rel_tol=0.0, max_iter=WG, mode="fast")
     x.zero_()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -276,7 +279,7 @@ def main():
     t_dev = ev0.elapsed_time(ev1) / 1e3
     value = n * K / t_dev / 1e9
     x.zero_()
-    hx.cg(A, b, x, rel_tol=0.0, max_iter=2, mode="reference")
+    hx.cg(A, b, x, rel_tol=0.0, max_iter=WG, mode="reference")
     x.zero_()
     torch.cuda.synchronize()
     ev0.record(st)
@@ -335,7 +338,7 @@ def main():
     repc = _lib.CGReportC()
     ws = op.workspace()
     ws.set_mode("fast")
-    L.hexbp_cg_host(setup._h, ws._h, C.cast(bh.data_ptr(), _dp), C.cast(xh.data_ptr(), _dp), n, 0.0, 2,
+    L.hexbp_cg_host(setup._h, ws._h, C.cast(bh.data_ptr(), _dp), C.cast(xh.data_ptr(), _dp), n, 0.0, WG,
                     1 if bp != 1 else 0, C.byref(repc), None)
     xh.zero_()
     torch.cuda.synchronize()
@@ -423,7 +426,7 @@ def p_sweep(bp: int, K: int, local: int, ps=(2, 3, 4, 5, 6, 8), dofs: float = 50
             A = hx.ConstrainedOperator(op) if bp != 1 else op
             b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda(local)
             x = torch.zeros_like(b)
-            hx.cg(A, b, x, 0.0, 3, mode="fast")
+            hx.cg(A, b, x, 0.0, 8, mode="fast")  # one graph block: capture before timing
             x.zero_()
             torch.cuda.synchronize()
             ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -458,7 +461,7 @@ def cg_to_tol(bp: int, p: int, local: int, dofs: float = 50_000_000, rel_tol: fl
         A = hx.ConstrainedOperator(op) if bp != 1 else op
         b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda(local)
         x = torch.zeros_like(b)
-        hx.cg(A, b, x, 0.0, 3, mode="fast")
+        hx.cg(A, b, x, 0.0, 8, mode="fast")  # one graph block: capture before timing
         x.zero_()
         torch.cuda.synchronize()
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -514,7 +517,7 @@ def fusion_compare(bp: int, p: int, K: int, local: int, dofs: float = 30_000_000
             torch.cuda.synchronize()
             t_apply = ea.elapsed_time(eb) / K
             x = torch.zeros_like(b)
-            hx.cg(A, b, x, 0.0, 3, mode=mode)
+            hx.cg(A, b, x, 0.0, 8, mode=mode)  # one graph block: capture before timing
             x.zero_()
             torch.cuda.synchronize()
             ea.record()

@@ -492,7 +492,8 @@ void hexbp_workspace_destroy(hexbp_workspace_t wh) {
     if (b) cudaFree(b);
   if (w.host_sc) cudaFreeHost(w.host_sc);
   if (w.copy_st) cudaStreamDestroy(w.copy_st);
-  if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
+  for (auto& cg : w.cg_graphs)
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
   if (w.graph_st) cudaStreamDestroy(w.graph_st);
   if (w.ev_g0) cudaEventDestroy(w.ev_g0);
   if (w.ev_g1) cudaEventDestroy(w.ev_g1);
@@ -702,10 +703,15 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
     // return at once); with a tolerance the host checks the stopping state
     // after every block, where the eager loop checks it
     const int con = (constrained ? 1 : 0) + (w.exact ? 2 : 0) + (w.fast_op ? 4 : 0) + (w.multipass ? 8 : 0);
-    if (!w.cg_graph || w.cg_graph_key[0] != xv || w.cg_graph_key[1] != pv || w.cg_graph_key[2] != apv ||
-        w.cg_graph_key[3] != diag || w.cg_graph_con != con) {
-      if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
-      w.cg_graph = nullptr;
+    const void* key[4] = {xv, pv, apv, diag};
+    Workspace::CgGraph* hit = nullptr;
+    for (auto& cg : w.cg_graphs)
+      if (cg.exec && cg.con == con && std::memcmp(cg.key, key, sizeof key) == 0) hit = &cg;
+    if (!hit) {
+      Workspace::CgGraph& slot = w.cg_graphs[w.cg_graph_next];
+      w.cg_graph_next = (w.cg_graph_next + 1) % 4;
+      if (slot.exec) cudaGraphExecDestroy(slot.exec);
+      slot.exec = nullptr;
       cudaError_t ge = cudaSuccess;
       if (!w.graph_st) ge = cudaStreamCreateWithFlags(&w.graph_st, cudaStreamNonBlocking);
       if (!ge && !w.ev_g0) ge = cudaEventCreateWithFlags(&w.ev_g0, cudaEventDisableTiming);
@@ -718,26 +724,25 @@ int pcg_run(hexbp_setup_t h, hexbp_workspace_t wh, const double* b, double* x, c
         ge = cudaStreamEndCapture(w.graph_st, &graph);
         if (!ge) ge = le;
       }
-      if (!ge) ge = cudaGraphInstantiate(&w.cg_graph, graph, 0);
+      if (!ge) ge = cudaGraphInstantiate(&slot.exec, graph, 0);
+      if (!ge) ge = cudaGraphUpload(slot.exec, w.graph_st);
       if (graph) cudaGraphDestroy(graph);
       if (ge) {  // no graph on this system / configuration: the eager loop
         cudaGetLastError();
-        if (w.cg_graph) cudaGraphExecDestroy(w.cg_graph);
-        w.cg_graph = nullptr;
+        if (slot.exec) cudaGraphExecDestroy(slot.exec);
+        slot.exec = nullptr;
         w.cg_graph_failed = 1;
       } else {
-        w.cg_graph_key[0] = xv;
-        w.cg_graph_key[1] = pv;
-        w.cg_graph_key[2] = apv;
-        w.cg_graph_key[3] = diag;
-        w.cg_graph_con = con;
+        std::memcpy(slot.key, key, sizeof key);
+        slot.con = con;
+        hit = &slot;
       }
     }
-    if (w.cg_graph) {
+    if (hit) {
       CK(cudaEventRecord(w.ev_g0, st));
       CK(cudaStreamWaitEvent(w.graph_st, w.ev_g0, 0));
       for (; k0 + kCgGraphBlock - 1 <= max_iter; k0 += kCgGraphBlock) {
-        CK(cudaGraphLaunch(w.cg_graph, w.graph_st));
+        CK(cudaGraphLaunch(hit->exec, w.graph_st));
         if (rel_tol > 0.0 && k0 + kCgGraphBlock - 1 < max_iter) {
           CK(cudaMemcpyAsync(w.host_sc, w.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, w.graph_st));
           CK(cudaStreamSynchronize(w.graph_st));

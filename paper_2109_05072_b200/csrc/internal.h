@@ -166,9 +166,13 @@ struct Workspace {
   // arguments the iteration's kernels take that can change between solves
   cudaStream_t graph_st = nullptr;
   cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
-  cudaGraphExec_t cg_graph = nullptr;
-  const void* cg_graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
-  int cg_graph_con = -1;
+  struct CgGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+    int con = -1;
+  };
+  CgGraph cg_graphs[4];  // a few argument sets (modes, vectors) stay captured
+  int cg_graph_next = 0;
   int cg_graph_failed = 0;
 };
 

@@ -351,7 +351,7 @@ def main():
 
     kinfo = ws.kernel_info()
     line = {
-        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": 1, "steps": K, "warmup": W, "warmup_iterations_run": WG,
         "ms_per_step": t_dev / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference bench RHS, bench.hpp:234-243; device-generated box mesh)",
         "config": {"workload": f"BP3-family bp{bp} Q_{p} box {dims[0]}x{dims[1]}x{dims[2]} elements, {n} DOFs, "

@@ -193,13 +193,14 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 // SK = TPC*1000000 + EO*100000 + R*100 + 10 + KC: KC element columns per CTA
 // (fills the warps when q^2 is small), R*8 a register cap (R = 0: 255), EO the
 // even-odd contractions (EOB above), TPC the thread-per-column kernel below
-// (BP1 p = 1; SK/10 % 100 is then its min CTAs per SM). The tens digit is 1:
+// (BP1 p = 1, 2; SK/10 % 10 is then its min CTAs per SM, SK/100 % 10 its cp.async
+// staging). The tens digit is 1:
 // one lane per pencil (splitting pencils over 2-4 lanes and double-buffered G
 // staging lost every sweep and were removed). Values: measured per p on a B200
 // (profiles/r1c_sk_sweep*.jsonl).
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
-  constexpr int mass[9] = {0, 1000000, 16, 100014, 100015, 100013, 100011, 100011, 100012};
+  constexpr int mass[9] = {0, 1000000, 1000100, 100014, 100015, 100013, 100011, 100011, 100012};
   // p = 7 BP3 / BP5 run the DMMA kernels; these entries serve HEXBP_NO_DMMA=1 setups
   constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 102011, 100011};
   constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 100011, 100011};
@@ -800,22 +801,47 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   ring_dot_finish<NT>(A, blockIdx.x, cdot, s_red);
 }
 
-// Thread-per-column element kernel for BP1 at p = 1 (n = 2, q = 3): one
-// thread marches one element column in z with the whole element in
-// registers -- 8 nodes, 27 quadrature values, the z-shared input and output
-// node planes carried across elements -- and no barrier per element (the
-// CTA-per-column kernel above pays five per element, which dominates at
-// p = 1). z-segments as in bp_apply_kernel; ring partials in the same
-// lateral layout (every p = 1 node is a ring node), so the consumers are
-// unchanged.
+// Thread-per-column element kernel for BP1 at p = 1, 2 (n = 2, 3; q = 3, 4):
+// one thread marches one element column in z with the element in registers
+// and no barrier per element (the CTA-per-column kernel above pays five per
+// element, which dominates at small p). The sum factorisation streams so that
+// only one (p+1) q^2 stage is live: per node plane k, x then y interpolation
+// (t[k][b][a]); per quadrature row (b, a), z interpolation, the mass factor
+// and z back into the same registers (t becomes r2); per node plane k, y then
+// x back, the z-carry and the stores. Every contraction sums in the plain
+// loop order, as the CTA kernel's plain form. z-segments as in
+// bp_apply_kernel; ring partials in the same lateral layout, so the consumers
+// are unchanged.
+//
+// STG: the next element's factor block and u planes are fetched by cp.async
+// into a per-thread shared-memory slot while this element computes (no
+// registers held by the loads in flight; the row a of the factors is
+// re-filled as soon as it has been read). Slot strides are odd in 16-byte
+// (factors) / 8-byte (u) units, so the per-lane accesses are conflict free.
 constexpr int TPC_T = 128;
 
-template <int P, int Q, int MB>
+template <int P, int Q>
+struct TpcSmem {
+  static constexpr int N2 = (P + 1) * (P + 1);
+  static constexpr int GS = (Q * Q * Q + 1) / 2 * 2;
+  static constexpr int GSP = (GS / 2) % 2 ? GS : GS + 2;  // doubles per thread: factor block
+  static constexpr int USP = (P * N2) | 1;                // doubles per thread: u planes 1..P
+  static constexpr int BYTES = TPC_T * (GSP + USP) * 8;
+};
+
+__device__ __forceinline__ void cp_async16_cg(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int P, int Q, int MB, int STG>
 __global__ void __launch_bounds__(TPC_T, MB)
     tpc_mass_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
-  constexpr int N = P + 1, N2 = N * N, Q3 = Q * Q * Q;
+  constexpr int N = P + 1, N2 = N * N, QQ = Q * Q, Q3 = QQ * Q;
   constexpr int GS = (Q3 + 1) / 2 * 2;
+  constexpr bool GROW = QQ % 2 == 0;  // a row g[a][.] of the factors is 16-byte aligned: stream it by rows
+  using S = TpcSmem<P, Q>;
   __shared__ double s_red[TPC_T / 32];
+  extern __shared__ double tsm[];
   if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
   const int ncta = (A.ncols + TPC_T - 1) / TPC_T;
   const int seg = blockIdx.x / ncta;
@@ -848,138 +874,190 @@ __global__ void __launch_bounds__(TPC_T, MB)
 #pragma unroll
   for (int l = 0; l < N2; ++l) carry[l] = 0.0;
   double dot = 0.0;
+  double* gslot = tsm + threadIdx.x * S::GSP;
+  double* uslot = tsm + TPC_T * S::GSP + threadIdx.x * S::USP;
+  auto issue_u = [&](int ez) {  // planes 1..P of element ez
+#pragma unroll
+    for (int k = 1; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+          cp_async8(smem_u32(uslot + (k - 1) * N2 + j * N + i),
+                    A.u + base + i + static_cast<long long>(A.Nx) * j + plane * (ez * P + k));
+  };
+  auto issue_g = [&](int ez, int a) {  // row a of element ez's factors (the whole block if !GROW)
+    constexpr int n16 = GROW ? QQ / 2 : GS / 2;
+    const double* src = Gcol + static_cast<long long>(ez) * GS + (GROW ? a * QQ : 0);
+    double* dst = gslot + (GROW ? a * QQ : 0);
+#pragma unroll
+    for (int m = 0; m < n16; ++m) cp_async16_cg(smem_u32(dst + 2 * m), src + 2 * m);
+  };
   load_plane(0, e0 * P);
+  if constexpr (STG) {  // groups in flight, in order: U(ez), G(ez) at the top of element ez
+    issue_u(e0);
+    cp_async_commit();
+#pragma unroll
+    for (int a = 0; a < (GROW ? Q : 1); ++a) issue_g(e0, a);
+    cp_async_commit();
+  }
   for (int ez = e0; ez < z_hi; ++ez) {
+    const bool nxt = ez + 1 < z_hi;
+    if constexpr (STG) {
+      cp_async_wait<1>();  // U(ez) has landed
 #pragma unroll
-    for (int k = 1; k < N; ++k) load_plane(k, ez * P + k);
-    double g[GS];
-    const double2* gp = reinterpret_cast<const double2*>(Gcol + static_cast<long long>(ez) * GS);
+      for (int k = 1; k < N; ++k)
 #pragma unroll
-    for (int m = 0; m < GS / 2; ++m) {
-      const double2 v = __ldg(gp + m);
-      g[2 * m] = v.x;
-      g[2 * m + 1] = v.y;
+        for (int l = 0; l < N2; ++l) uraw[k][l] = uslot[(k - 1) * N2 + l];
+      if (nxt) issue_u(ez + 1);
+      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int k = 1; k < N; ++k) load_plane(k, ez * P + k);
     }
-    // masked input (ConstrainedOperator: P u)
-    double u[N][N2];
+    const double* ge = Gcol + static_cast<long long>(ez) * GS;
+    double g[GROW ? 1 : GS];  // the whole block when its rows are not 16-byte aligned (p = 1)
+    if constexpr (!GROW && !STG) {  // issued before the forward contractions, which cover its latency
 #pragma unroll
-    for (int k = 0; k < N; ++k)
+      for (int m = 0; m < GS / 2; ++m) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(ge) + m);
+        g[2 * m] = v.x;
+        g[2 * m + 1] = v.y;
+      }
+    }
+    // per node plane: masked input (ConstrainedOperator: P u), x then y interpolation
+    double t[N][Q][Q];  // [k][b][a]
 #pragma unroll
-      for (int l = 0; l < N2; ++l)
-        u[k][l] = (bcxy(l % N, l / N) || zbc(ez * P + k)) ? 0.0 : uraw[k][l];
-    // interpolation to the quadrature points, x then y then z
-    double t1[N][N][Q];  // [k][j][a]
+    for (int k = 0; k < N; ++k) {
+      double u[N2];
 #pragma unroll
-    for (int k = 0; k < N; ++k)
-#pragma unroll
-      for (int j = 0; j < N; ++j)
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double s = 0.0;
-#pragma unroll
-          for (int i = 0; i < N; ++i) s = fma(bs.B[a][i], u[k][j * N + i], s);
-          t1[k][j][a] = s;
-        }
-    double t2[N][Q][Q];  // [k][b][a]
-#pragma unroll
-    for (int k = 0; k < N; ++k)
-#pragma unroll
-      for (int b = 0; b < Q; ++b)
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) s = fma(bs.B[b][j], t1[k][j][a], s);
-          t2[k][b][a] = s;
-        }
-    double v[Q][Q][Q];  // [c][b][a] times the mass factor (operator.hpp:139-142)
-#pragma unroll
-    for (int c = 0; c < Q; ++c)
-#pragma unroll
-      for (int b = 0; b < Q; ++b)
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) s = fma(bs.B[c][k], t2[k][b][a], s);
-          v[c][b][a] = s * g[a * Q * Q + (b + Q * c)];  // device layout [a][b + q c] (setup.cu)
-        }
-    // back: z, y, x
-    double r2[N][Q][Q];
-#pragma unroll
-    for (int k = 0; k < N; ++k)
-#pragma unroll
-      for (int b = 0; b < Q; ++b)
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double s = 0.0;
-#pragma unroll
-          for (int c = 0; c < Q; ++c) s = fma(bs.B[c][k], v[c][b][a], s);
-          r2[k][b][a] = s;
-        }
-    double r1[N][N][Q];
-#pragma unroll
-    for (int k = 0; k < N; ++k)
+      for (int l = 0; l < N2; ++l) u[l] = (bcxy(l % N, l / N) || zbc(ez * P + k)) ? 0.0 : uraw[k][l];
+      double t1[N][Q];  // [j][a]
 #pragma unroll
       for (int j = 0; j < N; ++j)
 #pragma unroll
         for (int a = 0; a < Q; ++a) {
           double s = 0.0;
 #pragma unroll
-          for (int b = 0; b < Q; ++b) s = fma(bs.B[b][j], r2[k][b][a], s);
-          r1[k][j][a] = s;
+          for (int i = 0; i < N; ++i) s = fma(bs.B[a][i], u[j * N + i], s);
+          t1[j][a] = s;
         }
-    double o[N][N2];
 #pragma unroll
-    for (int k = 0; k < N; ++k)
+      for (int b = 0; b < Q; ++b)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) s = fma(bs.B[b][j], t1[j][a], s);
+          t[k][b][a] = s;
+        }
+    }
+    if constexpr (STG) cp_async_wait<1>();  // G(ez) has landed (U(ez + 1) may not have)
+    if constexpr (!GROW && STG) {
+#pragma unroll
+      for (int m = 0; m < GS / 2; ++m) {
+        const double2 v = reinterpret_cast<const double2*>(gslot)[m];
+        g[2 * m] = v.x;
+        g[2 * m + 1] = v.y;
+      }
+      if (nxt) issue_g(ez + 1, 0);
+    }
+    // per quadrature row (b, a): z interpolation, times the mass factor
+    // (operator.hpp:139-142; device layout g[a][b + q c], setup.cu), z back
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      double gr[GROW ? QQ : 1];
+      if constexpr (GROW) {
+#pragma unroll
+        for (int m = 0; m < QQ / 2; ++m) {
+          const double2 v = STG ? reinterpret_cast<const double2*>(gslot + a * QQ)[m]
+                                : __ldg(reinterpret_cast<const double2*>(ge + a * QQ) + m);
+          gr[2 * m] = v.x;
+          gr[2 * m + 1] = v.y;
+        }
+        if (STG && nxt) issue_g(ez + 1, a);  // the row has been read: refill it with the next element's
+      }
+#pragma unroll
+      for (int b = 0; b < Q; ++b) {
+        double v[Q];
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(bs.B[c][k], t[k][b][a], s);
+          v[c] = s * (GROW ? gr[b + Q * c] : g[a * QQ + b + Q * c]);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < Q; ++c) s = fma(bs.B[c][k], v[c], s);
+          t[k][b][a] = s;
+        }
+      }
+    }
+    if constexpr (STG) cp_async_commit();
+    // per node plane: y then x back, z-carry, transpose restriction part 1
+    // (every footprint node but the p = 2 centre is a ring node)
+    const int kend = (ez == A.nz - 1) ? N : P;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double r1[N][Q];  // [j][a]
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int b = 0; b < Q; ++b) s = fma(bs.B[b][j], t[k][b][a], s);
+          r1[j][a] = s;
+        }
+      double o[N2];
 #pragma unroll
       for (int j = 0; j < N; ++j)
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           double s = 0.0;
 #pragma unroll
-          for (int a = 0; a < Q; ++a) s = fma(bs.B[a][i], r1[k][j][a], s);
-          o[k][j * N + i] = s;
+          for (int a = 0; a < Q; ++a) s = fma(bs.B[a][i], r1[j][a], s);
+          o[j * N + i] = s;
         }
-    // transpose restriction, part 1: z-carry, then every footprint node is a ring node
+      if (k == 0) {
 #pragma unroll
-    for (int l = 0; l < N2; ++l) {
-      o[0][l] += carry[l];
-      carry[l] = o[P][l];
-    }
-    const int kend = (ez == A.nz - 1) ? N : P;
-    if (valid && ez >= z_lo) {
+        for (int l = 0; l < N2; ++l) o[l] += carry[l];
+      }
+      if (k == P) {  // the top plane is the next element's bottom plane
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (k < kend) {
-          const int Z = ez * P + k;
+        for (int l = 0; l < N2; ++l) carry[l] = o[l];
+      }
+      if (valid && ez >= z_lo && k < kend) {
+        const int Z = ez * P + k;
 #pragma unroll
-          for (int j = 0; j < N; ++j)
+        for (int j = 0; j < N; ++j)
 #pragma unroll
-            for (int i = 0; i < N; ++i) {
-              const int l = j * N + i;
-              const bool ring = i == 0 || i == P || j == 0 || j == P;
-              const double val = o[k][l];
-              if (ring) {
-                bool is_y = false;
-                const long long li = lat_store_index(L, P, A.nx, ex, ey, i, j, Z, is_y);
-                (is_y ? A.lateral : A.lat_x)[li] = val;
-                if (do_dot) {
-                  const double uv = uraw[k][l];
-                  if (bcxy(i, j) || zbc(Z)) {
-                    if (ring_owner(P, i, j, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0)) dot = fma(uv, uv, dot);
-                  } else {
-                    dot = fma(uv, val, dot);
-                  }
+          for (int i = 0; i < N; ++i) {
+            const int l = j * N + i;
+            const bool ring = i == 0 || i == P || j == 0 || j == P;
+            const double val = o[l];
+            if (ring) {
+              bool is_y = false;
+              const long long li = lat_store_index(L, P, A.nx, ex, ey, i, j, Z, is_y);
+              (is_y ? A.lateral : A.lat_x)[li] = val;
+              if (do_dot) {
+                const double uv = uraw[k][l];
+                if (bcxy(i, j) || zbc(Z)) {
+                  if (ring_owner(P, i, j, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0)) dot = fma(uv, uv, dot);
+                } else {
+                  dot = fma(uv, val, dot);
                 }
-              } else {
-                const long long node = base + i + static_cast<long long>(A.Nx) * j + plane * Z;
-                const double w = zbc(Z) ? uraw[k][l] : val;
-                A.w[node] = w;
-                if (do_dot) dot = fma(uraw[k][l], w, dot);
               }
+            } else {
+              const long long node = base + i + static_cast<long long>(A.Nx) * j + plane * Z;
+              const double w = zbc(Z) ? uraw[k][l] : val;
+              A.w[node] = w;
+              if (do_dot) dot = fma(uraw[k][l], w, dot);
             }
-        }
+          }
       }
     }
     // the top input plane is the next element's bottom plane
@@ -1079,7 +1157,8 @@ KInfo info_sel(int sk) {
   if constexpr (I < L::n) {
     constexpr int c = L::v[I];
     if constexpr (c / 1000000 % 10) {  // thread-per-column kernel
-      if (sk == c) return {reinterpret_cast<void*>(&tpc_mass_kernel<P, Q, c / 10 % 100>), TPC_T, 0, TPC_T};
+      if (sk == c) return {reinterpret_cast<void*>(&tpc_mass_kernel<P, Q, c / 10 % 10, c / 100 % 10>), TPC_T,
+                              c / 100 % 10 ? TpcSmem<P, Q>::BYTES : 0, TPC_T};
     } else {
       using K = Cfg<P, Q, KIND, c>;
       if (sk == c) return {kernel_ptr<P, Q, KIND, c>(), K::NT, K::SMEM_BYTES, K::KC};
@@ -1112,7 +1191,7 @@ void fill_eo(const double (&M)[Q][N], EOB<N, Q>& e) {
 
 template <int P, int Q, int KIND, int SK>
 cudaError_t launch_tpc(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static_assert(KIND == KIND_MASS && P == 1, "thread-per-column kernel: BP1, p = 1");
+  static_assert(KIND == KIND_MASS && P <= 2, "thread-per-column kernel: BP1, p = 1, 2");
   BasisT<P, Q> bs;
   for (int i = 0; i < Q; ++i)
     for (int j = 0; j <= P; ++j) {
@@ -1120,13 +1199,17 @@ cudaError_t launch_tpc(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
       bs.D[i][j] = s.D[i * (P + 1) + j];
     }
   static int occ = 0;
-  constexpr int MB = SK / 10 % 100;  // min CTAs per SM (register cap)
+  constexpr int MB = SK / 10 % 10;   // min CTAs per SM (register cap)
+  constexpr int STG = SK / 100 % 10;  // cp.async staging of the next element (TpcSmem)
+  constexpr int SMEM = STG ? TpcSmem<P, Q>::BYTES : 0;
+  static std::atomic<uint64_t> configured{0};
+  if (STG) set_smem_attr_once(configured, reinterpret_cast<const void*>(&tpc_mass_kernel<P, Q, MB, STG>), SMEM);
   if (occ == 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tpc_mass_kernel<P, Q, MB>, TPC_T, 0) != cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tpc_mass_kernel<P, Q, MB, STG>, TPC_T, SMEM) != cudaSuccess)
     occ = 1;
   const int ncta = (a.ncols + TPC_T - 1) / TPC_T;
   const int nseg = z_segments(ncta, occ, a.nz);
-  tpc_mass_kernel<P, Q, MB><<<ncta * nseg, TPC_T, 0, st>>>(a, bs, nseg);
+  tpc_mass_kernel<P, Q, MB, STG><<<ncta * nseg, TPC_T, SMEM, st>>>(a, bs, nseg);
   return cudaGetLastError();
 }
 

@@ -65,7 +65,11 @@ int hexbp_device_count(void);
 /* Replaces make_setup(kind, mesh) for the reference's structured box mesh
  * (operator.hpp:70-77, mesh.hpp:86-123, geometry.hpp:78-193): the mesh
  * coordinates, Jacobians and geometric factors are generated ON THE DEVICE
- * with the reference's operation order. extent = NULL means {1,1,1}. */
+ * with the reference's operation order. extent = NULL means {1,1,1}.
+ * Degrees: p = 1..8 run the fused kernels; p = 9, 10 (the reference accepts
+ * any p, basis.hpp:86-111) run the multipass pipeline in reference
+ * arithmetic -- their workspaces are created on HEXBP_BACKEND_MULTIPASS and
+ * accept HEXBP_MODE_REFERENCE only; p > 10 is HEXBP_INVALID_ARGUMENT. */
 int hexbp_setup_create_box(int bp, int p, const int dims[3], const double extent[3], double amplitude,
                            int device, hexbp_setup_t* out);
 

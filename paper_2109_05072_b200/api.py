@@ -366,6 +366,9 @@ def _check_device_vec(t, n: int, name: str):
         raise ValueError(f"{name}: L-vector length mismatch")
 
 
+FUSED_MAX_DEGREE = 8  # the fused kernels' degrees; 9..10 run the multipass pipeline (reference arithmetic)
+
+
 class OperatorHandle:
     """OperatorHandle (operator.hpp:244-420) bound to the CUDA backend."""
 
@@ -501,8 +504,8 @@ def cg(apply_op, b, x, rel_tol: float = 1e-8, max_iter: int = 2000, diag=None,
     else:
         raise TypeError("cg: expected an OperatorHandle or ConstrainedOperator of the CUDA backend")
     ws = ws or op.workspace()
-    if op.backend() == Backend.CudaMultipass:
-        mode = "reference"  # the multipass pipeline runs in reference arithmetic
+    if op.backend() == Backend.CudaMultipass or op.setup().p > FUSED_MAX_DEGREE:
+        mode = "reference"  # the multipass pipeline (and every degree > 8) runs in reference arithmetic
     ws.set_mode(mode)
     n = op.size()
     rep = _lib.CGReportC()

@@ -1337,6 +1337,10 @@ void apply_kernel_info(const Setup& s, int* regs, int* smem, int* threads, int* 
     return;
   }
   const KInfo ki = info_for(s);
+  if (ki.fn == nullptr) {  // generic degree (multipass pipeline): no single element kernel
+    *regs = *smem = *threads = *blocks_per_sm = 0;
+    return;
+  }
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, ki.fn);
   *regs = fa.numRegs;

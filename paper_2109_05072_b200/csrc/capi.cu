@@ -33,7 +33,7 @@ int default_q(int bp, int p) { return bp == 5 ? p + 1 : p + 2; }  // operator.hp
 
 int init_setup(Setup& s, int bp, int p, const int gdims[3], int z0, int z1, int device) {
   if (!(bp == 1 || bp == 3 || bp == 5)) return invalid("setup: bp must be 1, 3 or 5");
-  if (p < 1 || p > kMaxP) return invalid("setup: degree must be in [1, 8] for the device kernels");
+  if (p < 1 || p > kMaxPG) return invalid("setup: degree must be in [1, 10] for the device kernels");
   for (int d = 0; d < 3; ++d)
     if (gdims[d] < 1) return invalid("build_box_mesh: element counts must be >= 1");
   if (z0 < 0 || z1 <= z0 || z1 > gdims[2]) return invalid("setup: bad slab range");
@@ -467,6 +467,13 @@ int hexbp_workspace_create(hexbp_setup_t h, hexbp_workspace_t* out) {
   if (e) {
     hexbp_workspace_destroy(wh);
     return cuda_status(e, "workspace allocation");
+  }
+  if (s.p > kMaxP) {  // generic degree: the fused kernels stop at p = 8; the multipass pipeline serves it
+    const int rc = hexbp_workspace_set_backend(wh, HEXBP_BACKEND_MULTIPASS);
+    if (rc) {
+      hexbp_workspace_destroy(wh);
+      return rc;
+    }
   }
   *out = wh;
   return HEXBP_OK;
@@ -917,7 +924,8 @@ int hexbp_workspace_set_mode(hexbp_workspace_t wh, int mode) {
   if (!wh || (mode != HEXBP_MODE_REFERENCE && mode != HEXBP_MODE_FAST && mode != HEXBP_MODE_FAST_OPERATOR))
     return invalid("bad arithmetic mode");
   if (wh->w.multipass && mode != HEXBP_MODE_REFERENCE)
-    return invalid("the multipass backend runs in reference arithmetic only");
+    return invalid(wh->w.s->p > kMaxP ? "degree > 8 runs the multipass pipeline, in reference arithmetic only"
+                                      : "the multipass backend runs in reference arithmetic only");
   wh->w.exact = mode != HEXBP_MODE_FAST;
   wh->w.fast_op = mode == HEXBP_MODE_FAST_OPERATOR;
   return HEXBP_OK;
@@ -926,6 +934,7 @@ int hexbp_workspace_set_mode(hexbp_workspace_t wh, int mode) {
 int hexbp_workspace_set_backend(hexbp_workspace_t wh, int backend) {
   if (!wh || (backend != HEXBP_BACKEND_FUSED && backend != HEXBP_BACKEND_MULTIPASS)) return invalid("bad backend");
   Workspace& w = wh->w;
+  if (backend == HEXBP_BACKEND_FUSED && w.s->p > kMaxP) return invalid("the fused kernels take degrees 1..8");
   DeviceGuard g(w.device);
   if (backend == HEXBP_BACKEND_MULTIPASS && !w.mp_buf) {
     const size_t bytes = sizeof(double) * static_cast<size_t>(multipass_doubles(*w.s));

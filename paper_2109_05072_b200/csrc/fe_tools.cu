@@ -159,7 +159,7 @@ cudaError_t launch_interp_to_qpts(const Setup& s, const double* v, double* out, 
 cudaError_t launch_interp_transpose(const Setup& s, const double* vq, double* out, cudaStream_t st) {
   const FeCfg c = fe_cfg(s);
   const int n = c.n, q = c.q;
-  double Bt[kMaxQ * (kMaxP + 1)];
+  double Bt[kMaxQ * (kMaxPG + 1)];
   for (int a = 0; a < q; ++a)
     for (int i = 0; i < n; ++i) Bt[i * q + a] = s.B[a * n + i];
   double *dBt = nullptr, *we = nullptr;

@@ -32,8 +32,9 @@ inline void set_smem_attr_once(std::atomic<uint64_t>& mask, const void* fn, int 
   mask.fetch_or(bit, std::memory_order_release);
 }
 
-constexpr int kMaxP = 8;
-constexpr int kMaxQ = kMaxP + 2;
+constexpr int kMaxP = 8;            // the fused kernels (apply*.cu): p = 1..8, the BASELINE range
+constexpr int kMaxPG = 10;          // generic degrees 9..10: the multipass pipeline (multipass.cu)
+constexpr int kMaxQ = kMaxPG + 2;   // basis table storage
 
 // Device-resident CG state (solver.hpp:91-153); read/written only by kernels.
 struct DevScalars {
@@ -104,8 +105,8 @@ struct Setup {
   int device = 0;
   long long gstride = 0;
   int g_aos = 0;  // see ApplyArgs::g_aos; chosen per (kind, p) at setup (setup.cu)
-  double B[kMaxQ * (kMaxP + 1)] = {};
-  double D[kMaxQ * (kMaxP + 1)] = {};
+  double B[kMaxQ * (kMaxPG + 1)] = {};
+  double D[kMaxQ * (kMaxPG + 1)] = {};
   double qw[kMaxQ] = {};
   double* G = nullptr;  // device
   // box meshes (hexbp_setup_create_box*): the mesh parameters, so that node

@@ -50,8 +50,7 @@ __global__ void jacobi_elem_kernel(const JacCfg c, const double* __restrict__ G,
     g[t] = Ge[off];
   }
   __syncthreads();
-  const int l = threadIdx.x;
-  if (l >= nen) return;
+  for (int l = threadIdx.x; l < nen; l += blockDim.x) {
   const int i = l % n, j = (l / n) % n, k = l / (n * n);
   double sum = 0.0;
   for (int cc = 0; cc < q; ++cc)
@@ -74,6 +73,7 @@ __global__ void jacobi_elem_kernel(const JacCfg c, const double* __restrict__ G,
   // E-vector in the reference's element order e = ex + nx (ey + ny ez)
   const long long e = ex + static_cast<long long>(c.nx) * (ey + static_cast<long long>(c.ny) * ez);
   de[e * nen + l] = sum;
+  }
 }
 
 // scatter_add: each node sums its 1-8 element entries in ascending element
@@ -138,7 +138,7 @@ cudaError_t launch_jacobi_diagonal(const Setup& s, int constrained, double* diag
   if (!e) e = cudaFuncSetAttribute(&jacobi_elem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem));
   if (!e) {
-    const int threads = (nen + 31) / 32 * 32;
+    const int threads = nen < 1024 ? (nen + 31) / 32 * 32 : 1024;  // p >= 10: nodes strided over the CTA
     jacobi_elem_kernel<<<static_cast<unsigned>(s.E), threads, smem, st>>>(c, s.G, dB, dD, de);
     e = cudaGetLastError();
   }

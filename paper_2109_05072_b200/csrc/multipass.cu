@@ -220,7 +220,7 @@ cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u,
   double* dD = dB + q * n;
   double* dBt = dD + q * n;
   double* dDt = dBt + q * n;
-  double Bt[kMaxQ * (kMaxP + 1)], Dt[kMaxQ * (kMaxP + 1)];
+  double Bt[kMaxQ * (kMaxPG + 1)], Dt[kMaxQ * (kMaxPG + 1)];
   for (int a = 0; a < q; ++a)
     for (int i = 0; i < n; ++i) {
       Bt[i * q + a] = s.B[a * n + i];
@@ -236,8 +236,10 @@ cudaError_t launch_apply_multipass(const Setup& s, double* buf, const double* u,
   const size_t smg = sizeof(double) * (2 * q * n + nen + 2 * big * big * big + 3 * q3);
   const size_t smt = sizeof(double) * (2 * q * n + 3 * q3 + nen + 3 * big * big * big);
   static std::atomic<uint64_t> cfg_grad{0}, cfg_gradT{0};
+  // 100 KB covers both passes up to p = 10 (BP3: 82 / 96 KB)
   set_smem_attr_once(cfg_grad, reinterpret_cast<const void*>(&mp_grad_kernel), 100 * 1024);
   set_smem_attr_once(cfg_gradT, reinterpret_cast<const void*>(&mp_gradT_kernel), 100 * 1024);
+  if (smg > 100 * 1024 || smt > 100 * 1024) return cudaErrorInvalidValue;
   const int grid = 148 * 8;
   mp_gather_kernel<<<grid, 256, 0, st>>>(c, u, ue, s.E);
   mp_grad_kernel<<<static_cast<unsigned>(s.E), 256, smg, st>>>(c, dB, dD, ue, gq);

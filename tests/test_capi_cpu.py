@@ -88,4 +88,4 @@ def test_no_cpu_fallback_without_gpu():
 
 def test_invalid_setup_arguments():
     with pytest.raises(ValueError):
-        hx.make_setup(hx.BPKind.BP3, hx.HexMesh((2, 2, 2), 9))  # degree > 8: no device kernel
+        hx.make_setup(hx.BPKind.BP3, hx.HexMesh((2, 2, 2), 11))  # degree > 10: no device path

@@ -269,12 +269,17 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   // CTA = (column group, z-segment). A segment recomputes the element below
   // its first one without storing anything, so the carry hands it the full
   // bottom node plane and it owns that plane outright (no cross-CTA sum).
+  // The segments split the launch's element range [zr0, zr1) (the whole
+  // column, or a sub-range of the multi-GPU overlap, overlap.cu: a range that
+  // starts / ends inside the slab leaves its bottom / top plane as a share in
+  // carry_lo / carry_hi for launch_carry_combine -- no store, no dot).
   const int ncta = (A.ncols + KC - 1) / KC;
   const int seg = blockIdx.x / ncta;
   const int col0 = (blockIdx.x - seg * ncta) * KC;
   const int kv = A.ncols - col0 < KC ? A.ncols - col0 : KC;  // valid columns of this CTA
-  const int z_lo = static_cast<int>(static_cast<long long>(seg) * A.nz / nseg);
-  const int z_hi = static_cast<int>(static_cast<long long>(seg + 1) * A.nz / nseg);
+  const int zlen = A.zr1 - A.zr0;
+  const int z_lo = A.zr0 + static_cast<int>(static_cast<long long>(seg) * zlen / nseg);
+  const int z_hi = A.zr0 + static_cast<int>(static_cast<long long>(seg + 1) * zlen / nseg);
   const int e0 = seg > 0 ? z_lo - 1 : z_lo;
 
   // the basis (plain contractions): cB[a][i] = B(a, i), cD likewise
@@ -748,14 +753,20 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       // ---------------- transpose restriction, part 1 (see header)
       out[0] += carry;
       carry = out[P];  // the top plane is the next element's bottom plane
-      const int kend = (ez == A.nz - 1) ? N : P;
+      const bool lo_share = A.carry_lo != nullptr && ez == A.zr0;   // range starts inside the slab
+      const bool hi_share = A.carry_hi != nullptr && ez == A.zr1 - 1;  // range ends inside the slab
+      const int kend = (ez == A.nz - 1 || hi_share) ? N : P;
       const double* usz = Uz + (le & 1) * N * N * N;  // u of this element, still staged
+      const int kbeg = lo_share ? 1 : 0;
+      const int kstop = hi_share ? P : kend;
       if (zvalid && ez >= z_lo) {
+        if (lo_share) A.carry_lo[static_cast<long long>(col) * N * N + pz] = out[0];
+        if (hi_share) A.carry_hi[static_cast<long long>(col) * N * N + pz] = out[P];
         if (!do_dot) {  // plain apply: the lean epilogue
 #pragma unroll
           for (int r = 0; r < N; ++r) {
             const int k = r;
-            if (k < kend) {
+            if (k >= kbeg && k < kstop) {
               const int Z = ez * P + k;
               if (ring) {
                 lat[Z * lat_stride] = out[r];
@@ -772,7 +783,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
 #pragma unroll
           for (int r = 0; r < N; ++r) {
             const int k = r;
-            if (k < kend) {
+            if (k >= kbeg && k < kstop) {
               const int Z = ez * P + k;
               const double uv = usz[k * N * N];
               const bool zbc = CON && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi));
@@ -1233,7 +1244,9 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
                                                                 K::SMEM_BYTES) != cudaSuccess)
     occ = 1;
   const int ncta = (a.ncols + K::KC - 1) / K::KC;
-  const int nseg = z_segments(ncta, occ, a.nz);
+  int nseg = z_segments(ncta, occ, a.zr1 - a.zr0);
+  // a sub-range launch (overlap.cu) has ncols column-partial slots: at most KC segments
+  if ((a.zr0 != 0 || a.zr1 != a.nz) && nseg > K::KC) nseg = K::KC;
   const int f = (a.constrained ? 1 : 0) + (a.col_dot != nullptr ? 2 : 0);
   switch (f) {
 #define HXB_F(FF)                                                                                   \
@@ -1311,6 +1324,22 @@ cudaError_t launch_k(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+// Element ranges (ApplyArgs::zr0 / zr1, carry_lo / carry_hi) in the DFMA
+// element kernel: every degree but the thread-per-column BP1 p = 1, 2.
+bool dfma_ranges_supported(const Setup& s) {
+  const KInfo ki = info_for(s);
+  return ki.fn != nullptr && ki.cols != TPC_T;
+}
+
+cudaError_t launch_apply_dfma(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  switch (s.kind) {
+    case KIND_MASS: return launch_k<KIND_MASS>(s, a, st);
+    case KIND_DIFF: return launch_k<KIND_DIFF>(s, a, st);
+    case KIND_COLLOC: return launch_k<KIND_COLLOC>(s, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
 
 int fixup_grid(const Setup& s) {
   const long long P = s.p;

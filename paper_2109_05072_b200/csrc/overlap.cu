@@ -18,9 +18,10 @@
 //              single launch's -- then the same store / ring / p.Ap logic as
 //              the kernel's Z' epilogue (restriction.hpp:67-80 ordering).
 // The rank's p.Ap share: the three launches' partials and the combine's, in
-// fixed order (deterministic run to run). Both DMMA kernels take ranges (BP3
-// p = 7 and BP5 p = 7; BP5's p.Ap is the element energy form, so its combine
-// adds nothing to the dot).
+// fixed order (deterministic run to run). Both DMMA kernels (BP3 p = 7 and
+// BP5 p = 7; BP5's p.Ap is the element energy form, so its combine adds
+// nothing to the dot) and the DFMA element kernel (every other degree but the
+// thread-per-column BP1 p = 1, 2) take ranges.
 #include <cuda_runtime.h>
 
 #include "device_util.cuh"
@@ -30,6 +31,8 @@
 namespace hxb {
 
 bool use_mma(const Setup& s);
+bool dfma_ranges_supported(const Setup& s);                                       // apply.cu
+cudaError_t launch_apply_dfma(const Setup& s, const ApplyArgs& a, cudaStream_t st);  // apply.cu
 
 namespace {
 
@@ -107,10 +110,12 @@ __global__ void __launch_bounds__(CT) carry_combine_kernel(const __grid_constant
 }  // namespace
 
 bool apply_overlap_supported(const Setup& s) {
-  return use_mma(s) && (mma_kernel_applies(s) || mma5_kernel_applies(s)) && s.dims[2] >= 2;
+  const bool ranges = use_mma(s) ? (mma_kernel_applies(s) || mma5_kernel_applies(s)) : dfma_ranges_supported(s);
+  return ranges && s.dims[2] >= 2;
 }
 
 static cudaError_t launch_range(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
+  if (!use_mma(s)) return launch_apply_dfma(s, a, st);
   return mma5_kernel_applies(s) ? launch_apply_mma5(s, a, st) : launch_apply_mma(s, a, st);
 }
 
@@ -177,13 +182,18 @@ cudaError_t launch_carry_combine(const Setup& s, const Workspace& ws, const doub
   c.ticket = ob.tickets + 3;
   c.slots = ob.slots;
   c.nslots = 3;
-  c.nodal_dot = s.kind != KIND_COLLOC;
+  c.nodal_dot = !(use_mma(s) && mma5_kernel_applies(s));  // the BP5 DMMA kernel's p.Ap is the energy form
   c.out = out;
   const long long nodes = static_cast<long long>(c.nplanes) * s.dims[0] * s.dims[1] * (s.p + 1) * (s.p + 1);
   long long blocks = (nodes + CT - 1) / CT;
   if (blocks > kMaxCombineBlocks) blocks = kMaxCombineBlocks;
-  if (s.p != 7) return cudaErrorInvalidValue;  // the DMMA kernel (apply_overlap_supported)
-  carry_combine_kernel<7><<<static_cast<int>(blocks), CT, 0, st>>>(c);
+  switch (s.p) {
+#define HXB_CC(PP) \
+  case PP: carry_combine_kernel<PP><<<static_cast<int>(blocks), CT, 0, st>>>(c); break;
+    HXB_CC(1) HXB_CC(2) HXB_CC(3) HXB_CC(4) HXB_CC(5) HXB_CC(6) HXB_CC(7) HXB_CC(8)
+#undef HXB_CC
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -24,7 +24,12 @@ def _single(bp, p, dims, a, mode="fast"):
 
 
 @pytest.mark.parametrize("bp,p,dims", [(3, 7, (4, 3, 6)), (3, 7, (3, 4, 2)), (3, 7, (2, 2, 3)), (5, 7, (3, 3, 4)),
-                                       (5, 7, (2, 3, 2)), (5, 4, (3, 3, 4)), (1, 3, (3, 2, 3))])
+                                       (5, 7, (2, 3, 2)), (5, 4, (3, 3, 4)), (1, 3, (3, 2, 3)),
+                                       # DFMA degrees (element ranges in apply.cu), z-segmented interior
+                                       # ranges (BP3 p = 3: 3 columns per CTA, 8 interior layers), and the
+                                       # thread-per-column BP1 p = 2 (no ranges: the unsplit launch)
+                                       (3, 3, (2, 2, 10)), (3, 8, (2, 3, 3)), (3, 2, (4, 3, 5)), (5, 2, (2, 3, 4)),
+                                       (5, 5, (2, 2, 4)), (1, 8, (2, 2, 3)), (1, 5, (3, 2, 6)), (1, 2, (3, 3, 3))])
 @pytest.mark.parametrize("overlap", [True, False])
 def test_distributed_apply_is_the_single_gpu_apply(bp, p, dims, overlap):
     """Bit for bit: the split launches assemble the inner planes with the same
@@ -96,5 +101,24 @@ def test_distributed_bp5_dmma_cg(overlap):
     rep = dop.cg(b, x, rel_tol=1e-8, max_iter=3000, constrained=True)
     xs = torch.zeros_like(b)
     rs = hx.cg(hx.ConstrainedOperator(_single(5, 7, dims, a)), b, xs, 1e-8, 3000, mode="fast")
+    assert rep.converged and abs(rep.iterations - rs.iterations) <= 1
+    assert (torch.linalg.norm(x - xs) / torch.linalg.norm(xs)).item() <= 1e-8
+
+
+@pytest.mark.parametrize("bp,p,dims", [(3, 4, (4, 3, 6)), (1, 6, (3, 3, 4))])
+def test_distributed_dfma_cg(bp, p, dims):
+    """A DFMA degree's overlapped distributed solve (boundary / interior
+    element ranges) against the single-GPU fast solve."""
+    import torch
+
+    a = 0.1
+    con = bp != 1
+    dop = NcclSlabOperator(bp, p, dims, amplitude=a, overlap=True)
+    b = torch.from_numpy(hx.bench_rhs(bp, p, dims)).cuda()
+    x = torch.zeros_like(b)
+    rep = dop.cg(b, x, rel_tol=1e-8, max_iter=3000, constrained=con)
+    xs = torch.zeros_like(b)
+    op = _single(bp, p, dims, a)
+    rs = hx.cg(hx.ConstrainedOperator(op) if con else op, b, xs, 1e-8, 3000, mode="fast")
     assert rep.converged and abs(rep.iterations - rs.iterations) <= 1
     assert (torch.linalg.norm(x - xs) / torch.linalg.norm(xs)).item() <= 1e-8

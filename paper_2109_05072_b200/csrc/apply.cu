@@ -243,13 +243,15 @@ struct Cfg {
 };
 
 // F: bit 0 = ConstrainedOperator semantics (ApplyArgs::constrained), bit 1 =
-// the CG form with the fused p.Ap (ApplyArgs::col_dot) -- compile-time flags,
+// the CG form with the fused p.Ap (ApplyArgs::col_dot), bit 2 = a sub-range
+// launch with carry shares (the multi-GPU overlap) -- compile-time flags,
 // so neither costs tests (or registers) in the phase bodies (+1-5% over the
 // run-time flags across BP1/BP3/BP5 p = 2..8; BP1 p = 6, 8: -2%).
 template <int P, int Q, int KIND, int SK, int F = 3, typename K_ = Cfg<P, Q, KIND, SK>>
 __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     bp_apply_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<P, Q> bs, int nseg) {
   constexpr bool CON = (F & 1) != 0;
+  constexpr bool RNG = (F & 4) != 0;  // carry shares of a sub-range launch (overlap.cu)
   using K = Cfg<P, Q, KIND, SK>;
   constexpr int N = K::N, QQ = K::QQ, NT = K::NT, KC = K::KC;
   constexpr int NH = N / 2;
@@ -753,8 +755,8 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       // ---------------- transpose restriction, part 1 (see header)
       out[0] += carry;
       carry = out[P];  // the top plane is the next element's bottom plane
-      const bool lo_share = A.carry_lo != nullptr && ez == A.zr0;   // range starts inside the slab
-      const bool hi_share = A.carry_hi != nullptr && ez == A.zr1 - 1;  // range ends inside the slab
+      const bool lo_share = RNG && A.carry_lo != nullptr && ez == A.zr0;   // range starts inside the slab
+      const bool hi_share = RNG && A.carry_hi != nullptr && ez == A.zr1 - 1;  // range ends inside the slab
       const int kend = (ez == A.nz - 1 || hi_share) ? N : P;
       const double* usz = Uz + (le & 1) * N * N * N;  // u of this element, still staged
       const int kbeg = lo_share ? 1 : 0;
@@ -1247,7 +1249,8 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   int nseg = z_segments(ncta, occ, a.zr1 - a.zr0);
   // a sub-range launch (overlap.cu) has ncols column-partial slots: at most KC segments
   if ((a.zr0 != 0 || a.zr1 != a.nz) && nseg > K::KC) nseg = K::KC;
-  const int f = (a.constrained ? 1 : 0) + (a.col_dot != nullptr ? 2 : 0);
+  const int f = (a.constrained ? 1 : 0) + (a.col_dot != nullptr ? 2 : 0) +
+                (a.carry_lo != nullptr || a.carry_hi != nullptr ? 4 : 0);
   switch (f) {
 #define HXB_F(FF)                                                                                   \
   case FF: {                                                                                        \
@@ -1261,6 +1264,10 @@ cudaError_t launch_t(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
     HXB_F(1)
     HXB_F(2)
     HXB_F(3)
+    HXB_F(4)
+    HXB_F(5)
+    HXB_F(6)
+    HXB_F(7)
 #undef HXB_F
   }
   return cudaGetLastError();

@@ -218,6 +218,23 @@ struct SkList {
 #include HX_SK_SWEEP
 #endif
 
+// Column strides of the per-column scratch (CB) and of the staged G blocks
+// (GSM) when a CTA packs KC > 1 element columns: best_stride above makes one
+// column's pencil patterns conflict free, but the KC columns of a warp land
+// on the same banks when CB / GS are multiples of 16 apart. Pads chosen per
+// default (kind, p, KC) with an 8-byte-word bank model of all nine phase
+// accesses, each half-warp a separate request (wavefronts = the largest number
+// of distinct words on one bank; a whole-warp model mispredicted BP5 p = 2,
+// measured 13% slower with its pads): 3-44% fewer modelled shared-memory
+// wavefronts per element.
+// Encoded cb_pad * 100 + gs_pad (gs_pad even: 16-byte TMA destinations).
+constexpr int col_pad(int kind, int p, int kc) {
+  if (kind == 0) return p == 3 && kc == 4 ? 500 : p == 4 && kc == 5 ? 1312 : p == 5 && kc == 3 ? 400 : p == 8 && kc == 2 ? 512 : 0;
+  if (kind == 1) return p == 1 && kc == 7 ? 1108 : p == 2 && kc == 2 ? 1500 : p == 3 && kc == 3 ? 100 : p == 4 && kc == 2 ? 4 : 0;
+  return p == 1 && kc == 8 ? 404 : p == 2 && kc == 3 ? 1108 : p == 4 && kc == 3 ? 700 : p == 5 && kc == 2 ? 1004
+       : p == 6 && kc == 2 ? 900 : 0;
+}
+
 template <int P, int Q, int KIND, int SK>
 struct Cfg {
   static constexpr int N = P + 1;
@@ -233,11 +250,17 @@ struct Cfg {
   static constexpr int SB_IS = best_stride(N, Q, Q * Q, 1);
   static constexpr int SA_SIZE = FA * Q * SA_CS;
   static constexpr int SB_SIZE = FB * N * SB_IS;
-  static constexpr int CB = (SA_SIZE + SB_SIZE + 1) / 2 * 2;  // per-column scratch (A then B)
+#ifdef HX_NO_COL_PAD
+  static constexpr int PADC = 0;
+#else
+  static constexpr int PADC = KC > 1 ? col_pad(KIND, P, KC) : 0;
+#endif
+  static constexpr int CB = (SA_SIZE + SB_SIZE + 1) / 2 * 2 + PADC / 100;  // per-column scratch (A then B)
   static constexpr int COMP = KIND == KIND_MASS ? 1 : 6;
   static constexpr int GS = (COMP * Q * Q * Q + 1) / 2 * 2;  // element block of G (== Setup::gstride)
-  static constexpr int G_OFF = KC * CB;                      // 16-byte aligned TMA destinations
-  static constexpr int U_OFF = G_OFF + KC * GS;              // per column two u slabs (cp.async double buffer)
+  static constexpr int GSM = GS + PADC % 100;                // shared-memory stride of the staged G blocks
+  static constexpr int G_OFF = (KC * CB + 1) / 2 * 2;        // 16-byte aligned TMA destinations
+  static constexpr int U_OFF = G_OFF + KC * GSM;             // per column two u slabs (cp.async double buffer)
   static constexpr int BAR_OFF = U_OFF + KC * 2 * N * N * N;
   static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
 };
@@ -331,7 +354,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
   auto issue_g = [&](int ez) {  // thread 0
     mbar_arrive_expect_tx(bar, gbytes * kv);
     for (int kk = 0; kk < kv; ++kk)
-      bulk_g2s(smem_u32(smem + K::G_OFF + kk * K::GS), Gcta + kk * gcol + ez * K::GS, gbytes, bar, pol);
+      bulk_g2s(smem_u32(smem + K::G_OFF + kk * K::GSM), Gcta + kk * gcol + ez * K::GS, gbytes, bar, pol);
   };
   if (t == 0) {
     issue_g(e0);
@@ -497,7 +520,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
       const int it = act ? item : K::XI - 1;
       const int kx = it / QQ, pp = it % QQ;
       double* SB = smem + kx * K::CB + K::SA_SIZE;
-      const double* Ge = smem + K::G_OFF + kx * K::GS;
+      const double* Ge = smem + K::G_OFF + kx * K::GSM;
       if constexpr (MASS && K::EO) {
         double x0[N], v[Q], out[N];
 #pragma unroll

@@ -197,13 +197,13 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 // staging). The tens digit is 1:
 // one lane per pencil (splitting pencils over 2-4 lanes and double-buffered G
 // staging lost every sweep and were removed). Values: measured per p on a B200
-// (profiles/r1c_sk_sweep*.jsonl).
+// (profiles/r1c_sk_sweep*.jsonl; with the column pads: r2t_sk_kc_sweep.jsonl).
 constexpr int sk_default(int kind, int p) {
   // kind 0 = mass (Q = P+2), 1 = diffusion (Q = P+2), 2 = collocated (Q = P+1)
-  constexpr int mass[9] = {0, 1000000, 1000100, 100014, 100015, 100013, 100011, 100011, 100012};
+  constexpr int mass[9] = {0, 1000000, 1000100, 100014, 100015, 100013, 100012, 100011, 100012};
   // p = 7 BP3 / BP5 run the DMMA kernels; these entries serve HEXBP_NO_DMMA=1 setups
   constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 102011, 100011};
-  constexpr int coll[9] = {0, 18, 13, 12, 100013, 100012, 100012, 100011, 100011};
+  constexpr int coll[9] = {0, 18, 16, 12, 100013, 100012, 100012, 100011, 100011};
   return kind == 0 ? mass[p] : kind == 1 ? diff[p] : coll[p];
 }
 // Candidate codes compiled for (KIND, P); the first is the default. A sweep
@@ -227,12 +227,40 @@ struct SkList {
 // of distinct words on one bank; a whole-warp model mispredicted BP5 p = 2,
 // measured 13% slower with its pads): 3-44% fewer modelled shared-memory
 // wavefronts per element.
-// Encoded cb_pad * 100 + gs_pad (gs_pad even: 16-byte TMA destinations).
+// Encoded cb_pad * 100 + gs_pad (gs_pad even: 16-byte TMA destinations), for
+// every KC a work-split sweep may pick (p <= 6; KC = 1 needs none: the
+// per-pencil strides of best_stride are already optimal under the model).
+constexpr short kColPad[3][9][9] = {  // [kind][p][KC], generated by tools/bank_model.py --table
+    {{0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 700, 1314, 0, 1100, 1100, 1114, 1100},
+     {0, 0, 500, 500, 500, 500, 500, 500, 500},
+     {0, 0, 500, 500, 500, 512, 500, 500, 500},
+     {0, 0, 1312, 1312, 1312, 1312, 1312, 1312, 1312},
+     {0, 0, 400, 400, 400, 100, 100, 100, 100},
+     {0, 0, 100, 100, 100, 100, 100, 100, 100},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0}},
+    {{0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 700, 1308, 4, 1108, 1104, 1108, 1108},
+     {0, 0, 1500, 1500, 1500, 1500, 1500, 1500, 1500},
+     {0, 0, 100, 100, 100, 112, 100, 100, 100},
+     {0, 0, 4, 4, 4, 504, 4, 4, 4},
+     {0, 0, 1100, 1100, 1100, 1100, 1100, 1100, 1100},
+     {0, 0, 900, 1100, 1100, 1100, 1100, 1100, 1100},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0}},
+    {{0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 4, 204, 404, 404, 104, 404, 404},
+     {0, 0, 1100, 1108, 1104, 1108, 1104, 1108, 1108},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 700, 700, 700, 712, 700, 700, 700},
+     {0, 0, 1004, 1004, 1004, 1004, 1004, 1004, 1004},
+     {0, 0, 900, 900, 900, 900, 900, 900, 900},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0}}};
 constexpr int col_pad(int kind, int p, int kc) {
-  if (kind == 0) return p == 3 && kc == 4 ? 500 : p == 4 && kc == 5 ? 1312 : p == 5 && kc == 3 ? 400 : p == 8 && kc == 2 ? 512 : 0;
-  if (kind == 1) return p == 1 && kc == 7 ? 1108 : p == 2 && kc == 2 ? 1500 : p == 3 && kc == 3 ? 100 : p == 4 && kc == 2 ? 4 : 0;
-  return p == 1 && kc == 8 ? 404 : p == 2 && kc == 3 ? 1108 : p == 4 && kc == 3 ? 700 : p == 5 && kc == 2 ? 1004
-       : p == 6 && kc == 2 ? 900 : 0;
+  if (kind == 0 && p == 8 && kc == 2) return 512;  // BP1 p = 8's default split (the table stops at p = 6)
+  return kind >= 0 && kind < 3 && p >= 0 && p < 9 && kc >= 0 && kc < 9 ? kColPad[kind][p][kc] : 0;
 }
 
 template <int P, int Q, int KIND, int SK>

@@ -78,13 +78,17 @@ def wf_half(addrs):
         tot+=max(cnt.values())
     return tot
 
-def table():
-    """col_pad codes (cb_pad * 100 + gs_pad) for the default work splits (sk_default)."""
+def table(all_kc=False):
+    """col_pad codes (cb_pad * 100 + gs_pad): the default work splits (sk_default),
+    or (--table) every p <= 6 and KC = 2..8 (apply.cu kColPad; several minutes)."""
     global wf
     cfgs={0:{3:4,4:5,5:3,8:2},1:{1:7,2:2,3:3,4:2},2:{1:8,2:3,3:2,4:3,5:2,6:2}}
+    if all_kc:
+        cfgs={k:{(P,KC):None for P in range(1,7) for KC in range(2,9) if KC*(P+1 if k==2 else P+2)**2<=1024} for k in range(3)}
     full=wf
     for kind,d in cfgs.items():
-        for P,KC in d.items():
+        for key in d:
+            P,KC=key if all_kc else (key,d[key])
             res=[]
             for c in range(16):
                 for g in range(0,16,2):
@@ -97,4 +101,5 @@ def table():
 
 
 if __name__=='__main__':
-    table()
+    import sys
+    table('--table' in sys.argv)

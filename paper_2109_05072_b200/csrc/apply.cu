@@ -192,9 +192,9 @@ __device__ __forceinline__ void eo_bwd(const EOB<N, Q>& m, const double (&v)[Q],
 // Work split of the element kernel, per (P, KIND), as a code
 // SK = TPC*1000000 + EO*100000 + R*100 + 10 + KC: KC element columns per CTA
 // (fills the warps when q^2 is small), R*8 a register cap (R = 0: 255), EO the
-// even-odd contractions (EOB above), TPC the thread-per-column kernel below
-// (BP1 p = 1, 2; SK/10 % 10 is then its min CTAs per SM, SK/100 % 10 its cp.async
-// staging). The tens digit is 1:
+// even-odd contractions (EOB above), TPC the thread-per-column kernels below
+// (BP1 p = 1, 2 and BP5 p = 1; SK/10 % 10 is then the min CTAs per SM, SK/100 % 10
+// the cp.async staging of the BP1 kernel). The tens digit is 1:
 // one lane per pencil (splitting pencils over 2-4 lanes and double-buffered G
 // staging lost every sweep and were removed). Values: measured per p on a B200
 // (profiles/r1c_sk_sweep*.jsonl; with the column pads: r2t_sk_kc_sweep.jsonl).
@@ -203,7 +203,7 @@ constexpr int sk_default(int kind, int p) {
   constexpr int mass[9] = {0, 1000000, 1000100, 100014, 100015, 100013, 100012, 100011, 100012};
   // p = 7 BP3 / BP5 run the DMMA kernels; these entries serve HEXBP_NO_DMMA=1 setups
   constexpr int diff[9] = {0, 17, 12, 13, 101612, 102111, 100011, 102011, 100011};
-  constexpr int coll[9] = {0, 18, 16, 12, 100013, 100012, 100012, 100011, 100011};
+  constexpr int coll[9] = {0, 1000020, 16, 12, 100013, 100012, 100012, 100011, 100011};
   return kind == 0 ? mass[p] : kind == 1 ? diff[p] : coll[p];
 }
 // Candidate codes compiled for (KIND, P); the first is the default. A sweep
@@ -1132,6 +1132,132 @@ __global__ void __launch_bounds__(TPC_T, MB)
   ring_dot_finish<TPC_T>(A, blockIdx.x, cdot, s_red);
 }
 
+// Thread-per-column kernel for BP5 at p = 1 (n = q = 2, GLL collocation:
+// the interpolation is the identity, operator.hpp:55): one thread marches one
+// element column; per element the 8 nodes, the three derivatives at the 8
+// points (2-term sums), the factors (48 doubles, 16-byte loads issued before
+// the derivatives), the fluxes and the transposed derivatives -- no shared
+// memory, no barrier. Layout, z-carry, ring partials and p.Ap as
+// tpc_mass_kernel.
+template <int MB>
+__global__ void __launch_bounds__(TPC_T, MB)
+    tpc_colloc_p1_kernel(const __grid_constant__ ApplyArgs A, const __grid_constant__ BasisT<1, 2> bs, int nseg) {
+  constexpr int P = 1, N = 2, N2 = 4, Q = 2, Q3 = 8, GS = 6 * Q3;
+  __shared__ double s_red[TPC_T / 32];
+  if (A.sc != nullptr && *(volatile int*)&A.sc->status != ST_RUNNING) return;
+  const int ncta = (A.ncols + TPC_T - 1) / TPC_T;
+  const int seg = blockIdx.x / ncta;
+  const int col_raw = (blockIdx.x - seg * ncta) * TPC_T + threadIdx.x;
+  const bool valid = col_raw < A.ncols;
+  const int col = valid ? col_raw : A.ncols - 1;
+  const int ex = col % A.nx, ey = col / A.nx;
+  const int z_lo = static_cast<int>(static_cast<long long>(seg) * A.nz / nseg);
+  const int z_hi = static_cast<int>(static_cast<long long>(seg + 1) * A.nz / nseg);
+  const int e0 = seg > 0 ? z_lo - 1 : z_lo;
+  const bool do_dot = A.col_dot != nullptr;
+  const long long plane = static_cast<long long>(A.Nx) * A.Ny;
+  const long long base = ex * P + static_cast<long long>(A.Nx) * (ey * P);
+  const LatLayout L(P, A.nx, A.ny);
+  const double* Gcol = A.G + static_cast<long long>(col) * A.nz * GS;
+  const double D00 = bs.D[0][0], D01 = bs.D[0][1], D10 = bs.D[1][0], D11 = bs.D[1][1];
+  auto d2 = [&](int a, double x0, double x1) { return a == 0 ? fma(D01, x1, D00 * x0) : fma(D11, x1, D10 * x0); };
+
+  auto bcxy = [&](int i, int j) {
+    const int X = ex * P + i, Y = ey * P + j;
+    return A.constrained && (X == 0 || X == A.Nx - 1 || Y == 0 || Y == A.Ny - 1);
+  };
+  auto zbc = [&](int Z) { return A.constrained && ((Z == 0 && A.bc_zlo) || (Z == A.Nz - 1 && A.bc_zhi)); };
+  double uraw[N][N2];  // [k][j * 2 + i]
+  auto load_plane = [&](int k, int Z) {
+#pragma unroll
+    for (int l = 0; l < N2; ++l) uraw[k][l] = A.u[base + (l & 1) + static_cast<long long>(A.Nx) * (l >> 1) + plane * Z];
+  };
+  double carry[N2] = {0.0, 0.0, 0.0, 0.0};
+  double dot = 0.0;
+  load_plane(0, e0 * P);
+  for (int ez = e0; ez < z_hi; ++ez) {
+    load_plane(1, ez * P + 1);
+    double g[GS];
+    const double2* gp = reinterpret_cast<const double2*>(Gcol + static_cast<long long>(ez) * GS);
+#pragma unroll
+    for (int m = 0; m < GS / 2; ++m) {
+      const double2 v = __ldg(gp + m);
+      g[2 * m] = v.x;
+      g[2 * m + 1] = v.y;
+    }
+    double u[N][N2];  // ConstrainedOperator: P u
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int l = 0; l < N2; ++l) u[k][l] = (bcxy(l & 1, l >> 1) || zbc(ez * P + k)) ? 0.0 : uraw[k][l];
+    // fluxes at the points (a, b, c) = nodes (i, j, k): G (gr, gs, gt), operator.hpp:129-131
+    double fr[N][N2], fs[N][N2], ft[N][N2];
+#pragma unroll
+    for (int c = 0; c < Q; ++c)
+#pragma unroll
+      for (int b = 0; b < Q; ++b)
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          const double gr = d2(a, u[c][b * 2], u[c][b * 2 + 1]);
+          const double gs = d2(b, u[c][a], u[c][2 + a]);
+          const double gt = d2(c, u[0][b * 2 + a], u[1][b * 2 + a]);
+          const double* ge = g + a * Q * Q + b + Q * c;  // component m at ge[m Q^3] (setup.cu)
+          const double g0 = ge[0], g1 = ge[Q3], g2 = ge[2 * Q3], g3 = ge[3 * Q3], g4 = ge[4 * Q3], g5 = ge[5 * Q3];
+          fr[c][b * 2 + a] = g0 * gr + g1 * gs + g2 * gt;
+          fs[c][b * 2 + a] = g1 * gr + g3 * gs + g4 * gt;
+          ft[c][b * 2 + a] = g2 * gr + g4 * gs + g5 * gt;
+        }
+    // transposed derivatives: out = Dx^T fr + Dy^T fs + Dz^T ft
+    double o[N][N2];
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = fma(bs.D[1][i], fr[k][j * 2 + 1], bs.D[0][i] * fr[k][j * 2]);
+          s = fma(bs.D[0][j], fs[k][i], s);
+          s = fma(bs.D[1][j], fs[k][2 + i], s);
+          s = fma(bs.D[0][k], ft[0][j * 2 + i], s);
+          s = fma(bs.D[1][k], ft[1][j * 2 + i], s);
+          o[k][j * 2 + i] = s;
+        }
+#pragma unroll
+    for (int l = 0; l < N2; ++l) {
+      o[0][l] += carry[l];
+      carry[l] = o[P][l];
+    }
+    const int kend = (ez == A.nz - 1) ? N : P;
+    if (valid && ez >= z_lo) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (k < kend) {
+          const int Z = ez * P + k;
+#pragma unroll
+          for (int l = 0; l < N2; ++l) {  // every p = 1 footprint node is a ring node
+            const int i = l & 1, j = l >> 1;
+            bool is_y = false;
+            const long long li = lat_store_index(L, P, A.nx, ex, ey, i, j, Z, is_y);
+            (is_y ? A.lateral : A.lat_x)[li] = o[k][l];
+            if (do_dot) {
+              const double uv = uraw[k][l];
+              if (bcxy(i, j) || zbc(Z)) {
+                if (ring_owner(P, i, j, ex, ey, A.nx, A.ny) && !(A.zlo_shared && Z == 0)) dot = fma(uv, uv, dot);
+              } else {
+                dot = fma(uv, o[k][l], dot);
+              }
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < N2; ++l) uraw[0][l] = uraw[P][l];
+  }
+  const double cdot = do_dot ? block_sum<TPC_T>(dot, s_red) : 0.0;
+  ring_dot_finish<TPC_T>(A, blockIdx.x, cdot, s_red);
+}
+
 // Transpose restriction, part 2, for plain applies: every ring node sums its
 // 1-4 column partials in ascending column order (ring.cuh). (CG fuses this
 // into its r-update, cg.cu; p.Ap is complete after part 1.)
@@ -1220,7 +1346,9 @@ KInfo info_sel(int sk) {
   using L = SkList<KIND, P>;
   if constexpr (I < L::n) {
     constexpr int c = L::v[I];
-    if constexpr (c / 1000000 % 10) {  // thread-per-column kernel
+    if constexpr (c / 1000000 % 10 && KIND == KIND_COLLOC) {  // thread-per-column kernel, BP5 p = 1
+      if (sk == c) return {reinterpret_cast<void*>(&tpc_colloc_p1_kernel<c / 10 % 10>), TPC_T, 0, TPC_T};
+    } else if constexpr (c / 1000000 % 10) {  // thread-per-column kernel
       if (sk == c) return {reinterpret_cast<void*>(&tpc_mass_kernel<P, Q, c / 10 % 10, c / 100 % 10>), TPC_T,
                               c / 100 % 10 ? TpcSmem<P, Q>::BYTES : 0, TPC_T};
     } else {
@@ -1255,7 +1383,8 @@ void fill_eo(const double (&M)[Q][N], EOB<N, Q>& e) {
 
 template <int P, int Q, int KIND, int SK>
 cudaError_t launch_tpc(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
-  static_assert(KIND == KIND_MASS && P <= 2, "thread-per-column kernel: BP1, p = 1, 2");
+  static_assert((KIND == KIND_MASS && P <= 2) || (KIND == KIND_COLLOC && P == 1),
+                "thread-per-column kernels: BP1 p = 1, 2; BP5 p = 1");
   BasisT<P, Q> bs;
   for (int i = 0; i < Q; ++i)
     for (int j = 0; j <= P; ++j) {
@@ -1264,6 +1393,15 @@ cudaError_t launch_tpc(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
     }
   static int occ = 0;
   constexpr int MB = SK / 10 % 10;   // min CTAs per SM (register cap)
+  if constexpr (KIND == KIND_COLLOC) {
+    if (occ == 0 &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tpc_colloc_p1_kernel<MB>, TPC_T, 0) != cudaSuccess)
+      occ = 1;
+    const int ncta = (a.ncols + TPC_T - 1) / TPC_T;
+    const int nseg = z_segments(ncta, occ, a.nz);
+    tpc_colloc_p1_kernel<MB><<<ncta * nseg, TPC_T, 0, st>>>(a, bs, nseg);
+    return cudaGetLastError();
+  } else {
   constexpr int STG = SK / 100 % 10;  // cp.async staging of the next element (TpcSmem)
   constexpr int SMEM = STG ? TpcSmem<P, Q>::BYTES : 0;
   static std::atomic<uint64_t> configured{0};
@@ -1275,6 +1413,7 @@ cudaError_t launch_tpc(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
   const int nseg = z_segments(ncta, occ, a.nz);
   tpc_mass_kernel<P, Q, MB, STG><<<ncta * nseg, TPC_T, SMEM, st>>>(a, bs, nseg);
   return cudaGetLastError();
+  }
 }
 
 template <int P, int Q, int KIND, int SK>
@@ -1384,7 +1523,7 @@ cudaError_t launch_k(const Setup& s, const ApplyArgs& a, cudaStream_t st) {
 }  // namespace
 
 // Element ranges (ApplyArgs::zr0 / zr1, carry_lo / carry_hi) in the DFMA
-// element kernel: every degree but the thread-per-column BP1 p = 1, 2.
+// element kernel: every degree but the thread-per-column BP1 p = 1, 2, BP5 p = 1.
 bool dfma_ranges_supported(const Setup& s) {
   const KInfo ki = info_for(s);
   return ki.fn != nullptr && ki.cols != TPC_T;

@@ -21,7 +21,7 @@
 // fixed order (deterministic run to run). Both DMMA kernels (BP3 p = 7 and
 // BP5 p = 7; BP5's p.Ap is the element energy form, so its combine adds
 // nothing to the dot) and the DFMA element kernel (every other degree but the
-// thread-per-column BP1 p = 1, 2) take ranges.
+// thread-per-column BP1 p = 1, 2 and BP5 p = 1) take ranges.
 #include <cuda_runtime.h>
 
 #include "device_util.cuh"

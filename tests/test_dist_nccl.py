@@ -27,9 +27,10 @@ def _single(bp, p, dims, a, mode="fast"):
                                        (5, 7, (2, 3, 2)), (5, 4, (3, 3, 4)), (1, 3, (3, 2, 3)),
                                        # DFMA degrees (element ranges in apply.cu), z-segmented interior
                                        # ranges (BP3 p = 3: 3 columns per CTA, 8 interior layers), and the
-                                       # thread-per-column BP1 p = 2 (no ranges: the unsplit launch)
+                                       # thread-per-column BP1 p = 2 and BP5 p = 1 (no ranges: the unsplit launch)
                                        (3, 3, (2, 2, 10)), (3, 8, (2, 3, 3)), (3, 2, (4, 3, 5)), (5, 2, (2, 3, 4)),
-                                       (5, 5, (2, 2, 4)), (1, 8, (2, 2, 3)), (1, 5, (3, 2, 6)), (1, 2, (3, 3, 3))])
+                                       (5, 5, (2, 2, 4)), (1, 8, (2, 2, 3)), (1, 5, (3, 2, 6)), (1, 2, (3, 3, 3)),
+                                       (5, 1, (3, 2, 4))])
 @pytest.mark.parametrize("overlap", [True, False])
 def test_distributed_apply_is_the_single_gpu_apply(bp, p, dims, overlap):
     """Bit for bit: the split launches assemble the inner planes with the same

@@ -258,6 +258,42 @@ constexpr short kColPad[3][9][9] = {  // [kind][p][KC], generated by tools/bank_
      {0, 0, 900, 900, 900, 900, 900, 900, 900},
      {0, 0, 0, 0, 0, 0, 0, 0, 0},
      {0, 0, 0, 0, 0, 0, 0, 0, 0}}};
+// Per-column stride pad of the u staging slabs (cp.async writes, phase-Z and
+// epilogue reads: pencil pz of column kz at kz (2 n^3 + pad) + k n^2 + pz),
+// the smallest pad minimising the same half-warp bank model.
+constexpr int u_pad_cost(int N, int KC, int pad) {
+  int total = 0;
+  const int zi = KC * N * N;
+  for (int h0 = 0; h0 < zi; h0 += 16)
+    for (int k = 0; k < N; ++k) {
+      int cnt[16] = {};
+      int deg = 0;
+      for (int t = h0; t < h0 + 16 && t < zi; ++t) {
+        const int w = (t / (N * N)) * (2 * N * N * N + pad) + k * N * N + t % (N * N);
+        const int b = ((w % 16) + 16) % 16;
+        if (++cnt[b] > deg) deg = cnt[b];
+      }
+      total += deg;
+    }
+  return total;
+}
+constexpr int u_pad(int N, int KC) {
+  int best = 0, bc = 1 << 30;
+  for (int pad = 0; pad < 16; ++pad) {
+    const int c = u_pad_cost(N, KC, pad);
+    if (c < bc) {
+      bc = c;
+      best = pad;
+    }
+  }
+  return best;
+}
+// Joint optimum of the pencil strides for BP5 p = 2 at six columns per CTA
+// (tools/bank_model.py with the strides free: 468 -> 390 modelled wavefronts
+// per element step); elsewhere best_stride's per-column choice is already
+// jointly optimal. Encoded sa_cs * 100 + sb_is, 0 = best_stride.
+constexpr int stride_override(int kind, int p, int kc) { return kind == 2 && p == 2 && kc == 6 ? 2217 : 0; }
+
 constexpr int col_pad(int kind, int p, int kc) {
   if (kind == 0 && p == 8 && kc == 2) return 512;  // BP1 p = 8's default split (the table stops at p = 6)
   return kind >= 0 && kind < 3 && p >= 0 && p < 9 && kc >= 0 && kc < 9 ? kColPad[kind][p][kc] : 0;
@@ -274,8 +310,13 @@ struct Cfg {
   static constexpr int NT = ((XI + 31) / 32) * 32;
   static constexpr int FA = KIND == KIND_MASS ? 1 : 2;  // fields in smem A ([f][c][j][i])
   static constexpr int FB = KIND == KIND_MASS ? 1 : 3;  // fields in smem B ([f][i][c][b])
-  static constexpr int SA_CS = best_stride(N, Q, N * N, 0);
-  static constexpr int SB_IS = best_stride(N, Q, Q * Q, 1);
+#ifdef HX_NO_COL_PAD
+  static constexpr int SOV = 0;
+#else
+  static constexpr int SOV = stride_override(KIND, P, KC);
+#endif
+  static constexpr int SA_CS = SOV ? SOV / 100 : best_stride(N, Q, N * N, 0);
+  static constexpr int SB_IS = SOV ? SOV % 100 : best_stride(N, Q, Q * Q, 1);
   static constexpr int SA_SIZE = FA * Q * SA_CS;
   static constexpr int SB_SIZE = FB * N * SB_IS;
 #ifdef HX_NO_COL_PAD
@@ -289,7 +330,12 @@ struct Cfg {
   static constexpr int GSM = GS + PADC % 100;                // shared-memory stride of the staged G blocks
   static constexpr int G_OFF = (KC * CB + 1) / 2 * 2;        // 16-byte aligned TMA destinations
   static constexpr int U_OFF = G_OFF + KC * GSM;             // per column two u slabs (cp.async double buffer)
-  static constexpr int BAR_OFF = U_OFF + KC * 2 * N * N * N;
+#ifdef HX_NO_COL_PAD
+  static constexpr int USTR = 2 * N * N * N;
+#else
+  static constexpr int USTR = 2 * N * N * N + (KC > 1 ? u_pad(N, KC) : 0);  // per-column u staging stride
+#endif
+  static constexpr int BAR_OFF = U_OFF + KC * USTR;
   static constexpr int SMEM_BYTES = (BAR_OFF + 1) * 8;
 };
 
@@ -389,7 +435,7 @@ __global__ void __launch_bounds__(K_::NT) __maxnreg__(K_::MAXREG)
     if (e0 + 1 < z_hi)
       for (int kk = 0; kk < kv; ++kk) prefetch_l2_bulk(Gcta + kk * gcol + (e0 + 1) * K::GS, gbytes);
   }
-  double* Uz = smem + K::U_OFF + kz * 2 * N * N * N + pz;  // this z-pencil's u staging (buffer 0)
+  double* Uz = smem + K::U_OFF + kz * K::USTR + pz;  // this z-pencil's u staging (buffer 0)
   auto fetch_u = [&](int ez, int buf) {
     if (zvalid) {
 #pragma unroll

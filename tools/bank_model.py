@@ -100,6 +100,17 @@ def table(all_kc=False):
             print(kind,P,KC,'half-warp wavefronts',base[0],'->',best[0],'code',best[2]*100+best[3] if best[0]<base[0] else 0)
 
 
+def u_staging(P, KC, UP):
+    """u staging slabs (cp.async write, phase-Z read, epilogue read): pencil pz
+    of column kz at kz (2 n^3 + UP) + k n^2 + pz (apply.cu u_pad)."""
+    N = P + 1; ZI = KC * N * N; s = 0
+    for w0 in range(0, ((ZI + 31) // 32) * 32, 32):
+        for k in range(N):
+            s += wf([(t // (N * N)) * (2 * N ** 3 + UP) + k * N * N + t % (N * N) if t < ZI else None
+                     for t in range(w0, w0 + 32)])
+    return 3 * s
+
+
 if __name__=='__main__':
     import sys
     table('--table' in sys.argv)

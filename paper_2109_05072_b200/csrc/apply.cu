@@ -290,9 +290,11 @@ constexpr int u_pad(int N, int KC) {
 }
 // Joint optimum of the pencil strides for BP5 p = 2 at six columns per CTA
 // (tools/bank_model.py with the strides free: 468 -> 390 modelled wavefronts
-// per element step); elsewhere best_stride's per-column choice is already
-// jointly optimal. Encoded sa_cs * 100 + sb_is, 0 = best_stride.
-constexpr int stride_override(int kind, int p, int kc) { return kind == 2 && p == 2 && kc == 6 ? 2217 : 0; }
+// per element step) and BP3 p = 1 at seven; elsewhere best_stride's
+// per-column choice is already jointly optimal. Encoded sa_cs * 100 + sb_is, 0 = best_stride.
+constexpr int stride_override(int kind, int p, int kc) {
+  return kind == 2 && p == 2 && kc == 6 ? 2217 : kind == 1 && p == 1 && kc == 7 ? 524 : 0;  // BP3 p = 1: 378 -> 324
+}
 
 constexpr int col_pad(int kind, int p, int kc) {
   if (kind == 0 && p == 8 && kc == 2) return 512;  // BP1 p = 8's default split (the table stops at p = 6)
